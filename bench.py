@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark of the fused acoustic FD time step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--order 2]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+A "step" is one leapfrog time step of the whole hot path (source injection,
+stencil with band rule, time update, receiver sampling -- all SURVEY.md 8(a)
+rows) over the configured grid.  value = grid-point updates per second
+(Gpts/s) over all ranks, timed with CUDA events on the stream the kernels run
+on, W untimed warm-up steps first, max over ranks.  The per-step working set
+(p, p_prev, K: 1.5 GiB for C3) is far larger than the 126 MB L2, so no flush
+is needed between steps (stated in config).
+
+--impl reference times the fp64 CPU oracle (the tier's reference arm) on a
+bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_POINT = 16.0   # read p, p_prev, K; write p_next (fp32), DESIGN.md section 5
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic(workload: str, order: int):
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(f"{workload}:o{order}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled (every 50 ms) during the
+    timed region by a streaming `nvidia-smi -lms` child process."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._p = None
+        self._t = None
+
+    def _reader(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.3)   # let the first samples arrive before the timed region
+        except Exception:
+            self._p = None
+        return self
+
+    def __exit__(self, *a):
+        if self._p is not None:
+            time.sleep(0.1)
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+            self._t.join(timeout=5)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].strip().lower() == "active"})
+        # "under load": samples at or above half the max clock (idle samples excluded)
+        load = [v for v in sm if mx and v >= 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_oracle_sample(wl, budget_s: float = 15.0):
+    """Time the fp64 oracle as it stands on the host cores on a bounded sample:
+    full-width planes of the workload's grid, steps chosen from a calibration
+    step so the sample takes ~budget_s seconds.  Returns (Gpts/s, cores, desc)."""
+    import oracle
+    oracle.build()
+    cores = oracle.max_threads()
+    vel = wl.vel()
+    src = [(s.idx, s.f, s.t0, s.amp) for s in wl.sources]
+    # calibration: 1 step
+    t0 = time.perf_counter()
+    oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, nthreads=cores)
+    t1 = time.perf_counter() - t0
+    steps = int(max(2, min(wl.steps, budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.run(vel, wl.h, wl.dt, wl.order, steps, src, nthreads=cores)
+    el = time.perf_counter() - t0
+    return wl.npts * steps / el / 1e9, cores, f"{wl.name} full grid {wl.dims}, {steps} steps, {cores} threads"
+
+
+def run_reference(args, wl):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    cores = oracle.max_threads()
+    # bounded per-step sample: nz_s full-width planes, sized for ~0.15 s per step
+    vel_full_dims = wl.dims
+    plane = int(np.prod(vel_full_dims[1:]))
+    nz_s = max(2 * (wl.order // 2) + 1, min(wl.dims[0], int(3.0e7 / plane) or 1))
+    dims_s = (nz_s,) + tuple(vel_full_dims[1:])
+    from workloads import velocity
+    vel = velocity(wl.model, dims_s, nz_global=wl.dims[0])
+    srcz = nz_s // 2
+    src = [((srcz,) + tuple(s.idx[1:]), s.f, s.t0, s.amp) for s in wl.sources]
+    P = np.zeros(dims_s)
+    Pm = np.zeros(dims_s)
+    for _ in range(args.warmup):
+        P, Pm, _ = oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, P0=P, Pm1=Pm, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        P, Pm, _ = oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, P0=P, Pm1=Pm, nthreads=cores)
+    el = time.perf_counter() - t0
+    npts = int(np.prod(dims_s))
+    value = npts * args.steps / el / 1e9
+    sample = f"{wl.name}: {nz_s} of {wl.dims[0]} planes ({dims_s}), 1 time step per bench step"
+    line = {
+        "impl": "reference", "metric": "grid-point updates/s (Gpts/s)", "value": value, "unit": "Gpts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
+                   "sample_grid": list(dims_s)},
+        "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU side
+def run_ours(args, wl):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2311_05038_b200 as fd
+    from paper_2311_05038_b200 import fd as fdm
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    # weak scaling: every rank runs the configured grid (N independent replicas
+    # until the slab-decomposed path lands)
+    vel = wl.vel()
+    stream = torch.cuda.Stream(device=dev)
+    sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream.cuda_stream,
+                        options={fd.FD_OPT_ASYNC: 1})
+    for s in wl.sources:
+        sim.add_source(s.idx, s.f, s.t0, s.amp)
+    sim.set_receivers(wl.receivers)
+    sim.step(args.warmup)
+    stream.synchronize()
+    launches0 = sim.info()["kernel_launches"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        sim.step(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    info = sim.info()
+    launches = info["kernel_launches"] - launches0
+    T = sim.traces()
+    finite = bool(np.all(np.isfinite(T)))
+    sim.close()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    gpts = wl.npts * args.steps * world / (ms / 1e3) / 1e9
+
+    # e2e through the public API with host buffers: create (H2D of the model),
+    # K steps, traces + final wavefield read back (D2H)
+    e2e = None
+    if args.no_e2e:
+        return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, None)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with fd.Simulation(vel, wl.h, wl.dt, wl.order) as s2:
+        for s in wl.sources:
+            s2.add_source(s.idx, s.f, s.t0, s.amp)
+        s2.set_receivers(wl.receivers)
+        s2.step(args.steps)
+        T2 = s2.traces()
+        W2 = s2.wavefield()
+    e2e_s = time.perf_counter() - t0
+    h2d = vel.nbytes + 8 * len(wl.receivers) * wl.ndim
+    d2h = T2.nbytes + W2.nbytes
+    e2e = {"value": wl.npts * args.steps * world / e2e_s / 1e9, "unit": "Gpts/s",
+           "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+           "seconds": e2e_s}
+    return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e)
+
+
+def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e):
+    peak, peak_src = _peaks()
+    achieved = BYTES_PER_POINT * wl.npts / (ms_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": _ncu_traffic(wl.name, wl.order), "peak_source": peak_src,
+            "algorithmic_bytes_per_point": BYTES_PER_POINT, "points_per_launch": wl.npts,
+            "kernel": "fused_step_kernel"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc = cpu_oracle_sample(wl, args.cpu_budget)
+        cpu = {"value": v, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": desc}
+    line = {
+        "metric": "grid-point updates/s (Gpts/s)", "value": gpts, "unit": "Gpts/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
+                   "dt": wl.dt, "h": wl.h, "receivers": len(wl.receivers), "sources": len(wl.sources),
+                   "l2": "no flush: per-step working set %.2f GB >> 126 MB L2" % (12.0 * wl.npts / 1e9),
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk.summary(), "traces_finite": finite,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--order", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    from workloads import config
+    wl = config(args.config, order=args.order)
+    if args.impl == "reference":
+        return run_reference(args, wl)
+    return run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,191 @@
+/*
+ * fd.h -- C ABI of the B200-native acoustic finite-difference hot path.
+ *
+ * The method (Hadjigeorgiou et al., arXiv 2311.05038, "An approach to
+ * performance portability through generic programming"):
+ *   Eq. 1: d2P/dt2 = v^2 (d2P/dx2 + d2P/dz2) + S(t),
+ *   discretised by Listing 3's WaveSimulator::run() body:
+ *   add_source; fd_pzz; fd_pxx; fd_time; swap(Pold,P); swap(P,Pnew).
+ * One fd_step = that body, i.e. the leapfrog update
+ *   p_next = 2 p - p_prev + (v dt)^2 Lap_h(p)     (with the band rule),
+ * executed on the GPU as ONE fused kernel per step.
+ * The readings of the paper's gaps (stencil order, boundary, source, receivers,
+ * precision, CFL, 3D) are DESIGN.md section 3, "R#n" below.
+ *
+ * Conventions for every function:
+ *   - returns fd_status; FD_OK (0) on success, a negative code otherwise, with a
+ *     human-readable detail in fd_last_error() (thread-local).  The library
+ *     never aborts the process.
+ *   - all host pointers are caller-owned; they are read or written only during
+ *     the call and never retained (the start/stop protocol of P:115-123:
+ *     inputs are copied in at creation, outputs copied out on request).
+ *   - arrays are row-major with the SLOWEST axis first: 2D (nz, nx), 3D
+ *     (nz, ny, nx); x is the fastest axis (R#11).  Grid indices are int64.
+ *   - one context must not be used from two threads at once; distinct contexts
+ *     are independent.
+ *   - after FD_ERR_CUDA / FD_ERR_NCCL the context is poisoned: only fd_destroy
+ *     is valid on it.
+ */
+#ifndef FD_H
+#define FD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fd_ctx fd_ctx; /* opaque; owns all device memory of one run */
+
+typedef enum {
+    FD_OK = 0,
+    FD_ERR_ARG = -1,      /* invalid argument (null pointer, bad ndim/order/dims/h/dt, v<=0 or non-finite, f<=0) */
+    FD_ERR_RANGE = -2,    /* a source/receiver index outside the (global) grid */
+    FD_ERR_UNSTABLE = -3, /* max(v) dt / h above the CFL limit of R#8 (message carries the ratio) */
+    FD_ERR_NOMEM = -4,    /* device or host allocation failed */
+    FD_ERR_CUDA = -5,     /* CUDA runtime/driver failure (context poisoned) */
+    FD_ERR_NCCL = -6,     /* NCCL failure or NCCL unavailable (context poisoned) */
+    FD_ERR_STATE = -7     /* call not valid in the current state (see each function) */
+} fd_status;
+
+enum { FD_FIELD_CUR = 0,   /* P^k after k steps (before the injection of w_k)          */
+       FD_FIELD_PREV = 1   /* P_mod^{k-1}: the previous field INCLUDING its injection  */
+};                         /*   (Listing 3 rotation: swap(Pold,P) after add_source) */
+
+enum { FD_FLAG_ALLOW_UNSTABLE = 1u /* skip the CFL refusal (S:553 --allow-unstable) */ };
+
+/* ------------------------------------------------------------------ setup */
+
+/* Create a single-GPU context on the current CUDA device.
+ *   ndim   2 or 3 (the paper is 2D; 3D adds d2/dy2 with the same rule, R#10)
+ *   dims   ndim extents, slow->fast; each >= order+1 (grid at least the stencil)
+ *   h      uniform grid spacing (one _dh; R#9), > 0
+ *   dt     time step (_dt), > 0
+ *   order  spatial order 2|4|6|8 of the central second differences (R#1, R#2)
+ *   vel    host, prod(dims) fp32 velocities, all finite and > 0; copied.
+ *          Stored on the device as K = (v dt / h)^2 / scale (computed in fp64,
+ *          rounded once), the only per-point coefficient of the update (R#7).
+ *   flags  FD_FLAG_ALLOW_UNSTABLE to skip the CFL check (R#8).
+ * Initial state: P^0 = P^-1 = 0 (R#12), no sources, no receivers, k = 0.
+ * Errors: FD_ERR_ARG, FD_ERR_UNSTABLE, FD_ERR_NOMEM, FD_ERR_CUDA.  On error *out = NULL. */
+fd_status fd_create(fd_ctx **out, int ndim, const int64_t *dims, double h, double dt,
+                    int order, const float *vel, uint32_t flags);
+
+/* Distributed (one process per GPU, z-slab decomposition). */
+typedef struct {
+    int rank, nranks;      /* this process's slab and the number of slabs             */
+    int device;            /* CUDA device ordinal to use (-1: the current device)     */
+    const void *nccl_id;   /* 128-byte ncclUniqueId from fd_nccl_get_unique_id on rank 0,
+                              broadcast by the caller (e.g. torch.distributed); may be
+                              NULL when nranks == 1                                    */
+    int vel_is_slab;       /* 0: vel holds the global model; 1: only this rank's planes
+                              [z0, z1) of fd_partition                                 */
+} fd_dist;
+
+/* Same as fd_create for the slab [z0, z1) = fd_partition(global_dims[0], nranks, rank).
+ * Source/receiver indices stay GLOBAL.  Halo exchange of r planes per face per step
+ * over NCCL send/recv.  Errors as fd_create, plus FD_ERR_NCCL. */
+fd_status fd_create_dist(fd_ctx **out, int ndim, const int64_t *global_dims, double h,
+                         double dt, int order, const float *vel, uint32_t flags,
+                         const fd_dist *dist);
+
+/* Pure: the owned z range of a slab.  nz split evenly, the first nz % nranks slabs
+ * get one extra plane.  FD_ERR_ARG if nranks < 1, rank outside [0,nranks), nz < nranks. */
+fd_status fd_partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *z1);
+
+/* Writes a fresh 128-byte ncclUniqueId to out128.  FD_ERR_NCCL if NCCL is unavailable. */
+fd_status fd_nccl_get_unique_id(void *out128);
+
+/* Register a point source (add_source; R#4, R#5): before the stencil of step k,
+ * P[idx] += amp * R(k dt) with the Ricker wavelet R(t) = (1 - 2 pi^2 f^2 (t-t0)^2)
+ * exp(-pi^2 f^2 (t-t0)^2), evaluated in fp64 and rounded once to fp32.
+ * Several sources (even at one point) add in registration order.  At most 16.
+ *   idx  ndim global indices, slow->fast.
+ * Errors: FD_ERR_ARG (null, f_peak_hz <= 0, non-finite t0/amp, too many sources),
+ *         FD_ERR_RANGE (idx outside the grid), FD_ERR_STATE (after the first fd_step). */
+fd_status fd_add_source(fd_ctx *ctx, const int64_t *idx, double f_peak_hz, double t0_s,
+                        double amp);
+
+/* Register receivers (R#6), replacing any previous set: trace sample k of receiver j is
+ * P^{k+1}[idx_j], the newest field after step k (before the injection of w_{k+1}).
+ *   idx  nrec x ndim global indices (row j = receiver j), slow->fast; nrec >= 0.
+ * Errors: FD_ERR_ARG, FD_ERR_RANGE, FD_ERR_STATE (after the first fd_step). */
+fd_status fd_set_receivers(fd_ctx *ctx, int64_t nrec, const int64_t *idx);
+
+/* ------------------------------------------------------------------- run */
+
+/* Advance n >= 0 time steps (n repetitions of the run() body, R#15).  Synchronous:
+ * returns after the device work is complete (or enqueued when a stream was set
+ * with fd_set_stream and FD_OPT_ASYNC is 1).  Errors: FD_ERR_ARG (n < 0),
+ * FD_ERR_CUDA, FD_ERR_NCCL, FD_ERR_NOMEM (trace buffer growth). */
+fd_status fd_step(fd_ctx *ctx, int64_t n);
+
+/* Copy a field to host_out (prod(local dims) floats; local = the slab in distributed
+ * mode, the whole grid otherwise).  which = FD_FIELD_CUR | FD_FIELD_PREV.
+ * Errors: FD_ERR_ARG, FD_ERR_CUDA. */
+fd_status fd_get_wavefield(fd_ctx *ctx, int which, float *host_out);
+
+/* Copy the traces recorded so far to host_out as a receiver-major nrec x nsteps matrix
+ * (row j = receiver j in registration order).  cap = capacity of host_out in floats;
+ * *nsteps_out = steps recorded.  In distributed mode rows of receivers owned by other
+ * ranks are exactly 0 (sum across ranks to assemble).
+ * Errors: FD_ERR_ARG (null), FD_ERR_STATE (no receivers, or cap < nrec*nsteps), FD_ERR_CUDA. */
+fd_status fd_get_traces(fd_ctx *ctx, float *host_out, int64_t cap, int64_t *nsteps_out);
+
+/* Release everything.  NULL -> FD_OK. */
+fd_status fd_destroy(fd_ctx *ctx);
+
+const char *fd_strerror(fd_status s); /* static string for a status code      */
+const char *fd_last_error(void);      /* thread-local detail of the last error */
+
+/* ------------------------------------------------------ interop and hooks */
+
+/* Launch all device work of ctx on this cudaStream_t (e.g. torch's current stream);
+ * NULL = the legacy default stream.  Errors: FD_ERR_ARG. */
+fd_status fd_set_stream(fd_ctx *ctx, void *cuda_stream);
+
+/* Process-global device allocator (e.g. torch's caching allocator); call before any
+ * fd_create.  alloc(bytes, user) returns device memory or NULL; free_(ptr, user).
+ * Passing NULL for both restores cudaMalloc/cudaFree.  Errors: FD_ERR_STATE if
+ * contexts are alive. */
+fd_status fd_set_allocator(void *(*alloc)(size_t bytes, void *user),
+                           void (*free_)(void *ptr, void *user), void *user);
+
+/* Test hook: set P^0 (which = FD_FIELD_CUR) or P^-1 (FD_FIELD_PREV) from host
+ * (prod(local dims) floats).  Only before the first fd_step, else FD_ERR_STATE. */
+fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
+
+/* Tuning / debug options; set before the first fd_step (else FD_ERR_STATE).
+ *   FD_OPT_KERNEL    0 auto (fused TMA kernel), 1 naive reference kernels (debug,
+ *                    three launches per step), 2 fused TMA kernel
+ *   FD_OPT_TILE      index into the compiled tile table (-1 = auto); see fd_get_info
+ *   FD_OPT_ZCHUNKS   z-chunks per x-y tile column (0 = auto)
+ *   FD_OPT_ASYNC     1: fd_step returns without synchronising the stream
+ *   FD_OPT_GRAPH     1: replay fd_step's launches from CUDA graphs (default 1)
+ *   FD_OPT_VSLABS    n >= 1: split the grid into n z-slabs on this one GPU with
+ *                    device-copy halo exchange (tests the slab logic)
+ * Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
+enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
+       FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6 };
+fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
+
+/* Introspection (bench / tests). */
+typedef struct {
+    int64_t steps_done;        /* k                                                     */
+    int64_t kernel_launches;   /* device kernels launched by this context so far         */
+    int64_t local_dims[3];     /* slow->fast (unused trailing entries 0)                 */
+    int64_t z0, z1;            /* owned global planes                                    */
+    int64_t pitch;             /* floats per stored row (>= nx, multiple of 32)          */
+    int kernel;                /* 1 naive, 2 fused TMA                                   */
+    int tile_x, tile_y, rows_per_thread, p_stages, k_stages;
+    int ctas, threads_per_cta, smem_bytes, zchunks;
+    int order;
+    double device_bytes;       /* bytes of device memory held                           */
+} fd_info;
+fd_status fd_get_info(fd_ctx *ctx, fd_info *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FD_H */

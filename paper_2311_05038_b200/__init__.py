@@ -1,0 +1,12 @@
+"""B200-native acoustic finite-difference hot path of arXiv 2311.05038.
+
+The product is the C-ABI library ``libfd.so`` (include/fd.h) built from
+``csrc/``; ``fd`` is its thin ctypes binding.  Importing this package loads the
+library and fails loudly if it is missing: there is no CPU fallback.
+"""
+from .fd import (  # noqa: F401
+    FD_FIELD_CUR, FD_FIELD_PREV, FD_FLAG_ALLOW_UNSTABLE, FD_OPT_ASYNC, FD_OPT_GRAPH, FD_OPT_KERNEL,
+    FD_OPT_TILE, FD_OPT_VSLABS, FD_OPT_ZCHUNKS, FDError, Simulation, fd_add_source, fd_create,
+    fd_create_dist, fd_destroy, fd_get_info, fd_get_traces, fd_get_wavefield, fd_nccl_get_unique_id,
+    fd_partition, fd_set_option, fd_set_receivers, fd_set_stream, fd_set_wavefield, fd_step, lib,
+)

@@ -1,0 +1,450 @@
+// fd_kernels.cuh -- sm_100a device code of the fused acoustic FD time step.
+//
+// One launch = one time step of Listing 3's run() body:
+//   add_source (eager form, see below) ; fd_pzz ; [fd_pyy] ; fd_pxx ; fd_time ;
+//   swap  (host pointer swap, zero bytes)
+// fused into one pass that reads p, p_prev, K once and writes p_next once
+// (16 B per grid-point update).
+//
+// Canonical per-point fp32 expression (every GPU variant evaluates exactly this,
+// which makes "fused == naive" and "N slabs == 1 slab" bitwise contracts):
+//   s_a = c0*p_i ; s_a = fma(c_m, p_{i-m e_a} + p_{i+m e_a}, s_a)  m = 1..r
+//   S   = [x in] s_x ; S = [y in] S + s_y ; S = [z in] S + s_z     (band rule, R#3)
+//   p_next_i = fma(K_i, S, fma(2, p_i, -p_prev_i))
+// with integer-scaled taps c (x1, x12, x180, x5040; the 1/scale is folded into
+// K = (v dt / h)^2 / scale, computed once on the host in fp64).
+//
+// Source injection is applied EAGERLY: the kernel of step k, after
+// computing p_next = P^{k+1} at a source point, stores the raw value (for
+// readback and receivers) and then adds w_{k+1} in registration order, so the
+// memory holds exactly the P that step k+1's add_source would produce.  This
+// is the same fp32 add on the same operands as in-place injection.
+//
+// Memory layout (HBM): each field buffer holds (nz_local + 2r) planes of
+// ny rows of `pitch` floats (pitch = nx rounded up to 32 floats = 128 B); plane
+// z of the slab lives at buffer plane z + r; the r planes on each side are
+// zero (single GPU / global faces) or halo copies (slabs).  K has nz_local
+// planes with the same pitch.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fdk {
+
+constexpr int kMaxSources = 16;
+
+// Integer-scaled central second-difference taps (R#2):
+// the exact rationals of order 2r multiplied by scale = 1, 12, 180, 5040.
+__host__ __device__ constexpr float tap(int R, int m) {
+    return R == 1 ? (m == 0 ? -2.f : 1.f)
+         : R == 2 ? (m == 0 ? -30.f : m == 1 ? 16.f : -1.f)
+         : R == 3 ? (m == 0 ? -490.f : m == 1 ? 270.f : m == 2 ? -27.f : 2.f)
+                  : (m == 0 ? -14350.f : m == 1 ? 8064.f : m == 2 ? -1008.f : m == 3 ? 128.f : -9.f);
+}
+__host__ __device__ constexpr double tap_scale(int R) {
+    return R == 1 ? 1.0 : R == 2 ? 12.0 : R == 3 ? 180.0 : 5040.0;
+}
+
+struct Receivers {
+    const int32_t *off;   // CSR offsets per work unit [nunits + 1] (fused kernel)
+    const int32_t *z;     // local plane
+    const int32_t *y;
+    const int32_t *x;
+    const int32_t *id;    // column in the step-major trace row
+};
+
+struct StepParams {
+    int64_t nx, ny, nz;     // local extents (nz = owned planes)
+    int64_t pitch;          // floats per row
+    int64_t gz0;            // global z of local plane 0
+    int64_t nzg;            // global nz (z band)
+    int32_t zlo, zhi;       // local planes computed by this launch
+    int32_t ntx, nty;       // tiles along x, y
+    int32_t nchunks;        // z-chunks of [zlo, zhi)
+    float *pnext;           // base of the p_prev buffer (overwritten in place)
+    const float *p;         // base of the p buffer (naive kernel only)
+    const float *K;         // K base (naive kernel only)
+    // eager source injection of w_{k+1}
+    int32_t nsrc;
+    int32_t sz[kMaxSources], sy[kMaxSources], sx[kMaxSources];   // local coords (sz may be outside)
+    float w[kMaxSources];
+    float *src_raw;         // [nsrc] raw p_next before the s-th injection
+    // receivers
+    Receivers rec;
+    int32_t nrec_local;     // receivers of this launch's list (naive gather)
+    float *trace_row;       // traces + k * nrec_total
+};
+
+// ------------------------------------------------------------------ PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
+                                            int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ float4 lds128(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+__device__ __forceinline__ float f4(const float4 &v, int e) {
+    return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void f4set(float4 &v, int e, float s) {
+    if (e == 0) v.x = s; else if (e == 1) v.y = s; else if (e == 2) v.z = s; else v.w = s;
+}
+
+// ------------------------------------------------------------ compile-time config
+// TMA boxes are at most 256 elements per dimension and their rows a multiple
+// of 16 B: a wide 2D row strip is fetched as `pieces(w)` equal boxes.
+constexpr int pieces(int w) {
+    for (int n = 1; n <= w; ++n)
+        if (w % n == 0 && (w / n) % 4 == 0 && w / n <= 256) return n;
+    return -1;
+}
+
+template <int R_, int NDIM_, int TX_, int TY_, int NY_, int DP_, int DK_>
+struct Cfg {
+    static constexpr int R = R_, NDIM = NDIM_, TX = TX_, TY = TY_, NY = NY_, DP = DP_, DK = DK_;
+    static constexpr int HY = (NDIM == 3) ? R : 0;                // y halo rows
+    static constexpr int BX = TX + 8;                             // x halo: 4-float aligned each side
+    static constexpr int BY = TY + 2 * HY;
+    static constexpr int NPP = pieces(BX), PBW = BX / NPP;       // p box: (PBW, BY, 1) x NPP
+    static constexpr int NTP = pieces(TX), TBW = TX / NTP;       // tile box: (TBW, TY, 1) x NTP
+    // TMA writes each box at a 128-B aligned SMEM address: multi-box rows (2D)
+    // place box i at i*PPAD floats; pcol() maps a tile column to its SMEM column
+    static constexpr int PPAD = (NPP == 1) ? BX : ((PBW + 31) / 32) * 32;
+    static constexpr int P_FLOATS = (((NPP == 1 ? BX * BY : NPP * PPAD)) + 31) / 32 * 32;
+    __device__ static constexpr int pcol(int c) { return NPP == 1 ? c : (c / PBW) * PPAD + c % PBW; }
+    static constexpr int T_FLOATS = TX * TY;
+    static constexpr int K_FLOATS = 2 * T_FLOATS;                 // p_prev tile + K tile
+    static constexpr uint32_t P_BYTES = BX * BY * 4;
+    static constexpr uint32_t T_BYTES = T_FLOATS * 4;
+    static constexpr int NSP = R + 1 + DP;                        // p-plane ring
+    static constexpr int NSK = DK + 1;                            // (p_prev, K) ring
+    static constexpr int NTX = TX / 4, NTY = TY / NY;
+    static constexpr int NCONS = NTX * NTY;
+    static constexpr int NWC = NCONS / 32;
+    static constexpr int NTHREADS = NCONS + 32;                   // + one producer warp
+    static constexpr int SMEM_FLOATS = NSP * P_FLOATS + NSK * K_FLOATS;
+    static constexpr int SMEM_BYTES = SMEM_FLOATS * 4 + (2 * NSP + 2 * NSK) * 8 + 16;
+    static_assert(TX % 4 == 0 && TY % NY == 0, "tile");
+    static_assert(NCONS % 32 == 0, "consumer threads must be whole warps");
+    static_assert(NPP > 0 && NTP > 0 && BY <= 256 && TY <= 256, "TMA box limit");
+    static_assert((NPP == 1 && NTP == 1) || BY == 1, "multi-box rows only for 1-row planes (2D)");
+    static_assert(R >= 1 && R <= 4, "r");
+};
+
+// ------------------------------------------------------------------ fused kernel
+// grid = ntx * nty * nchunks CTAs; CTA b handles tile (b % ntiles) of z-chunk
+// (b / ntiles) (chunk-major, so co-resident CTAs stream the same z region and
+// share x-y halos in L2).  Warp NWC is the TMA producer; warps 0..NWC-1 compute.
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS)
+fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, BY, 1)
+                  const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, TY, 1)
+                  const __grid_constant__ CUtensorMap map_k,    // K, box (TX, TY, 1)
+                  const StepParams prm) {
+    constexpr int R = C::R;
+    extern __shared__ __align__(128) float smem[];
+    float *sP = smem;                                   // NSP * P_FLOATS
+    float *sK = smem + C::NSP * C::P_FLOATS;            // NSK * K_FLOATS
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sK + C::NSK * C::K_FLOATS);
+    uint64_t *fullP = bars, *emptyP = bars + C::NSP;
+    uint64_t *fullK = bars + 2 * C::NSP, *emptyK = fullK + C::NSK;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int ntiles = prm.ntx * prm.nty;
+    const int unit = blockIdx.x;
+    const int chunk = unit / ntiles;
+    const int tile = unit - chunk * ntiles;
+    const int x0 = (tile % prm.ntx) * C::TX;
+    const int y0 = (tile / prm.ntx) * C::TY;
+    const int span = prm.zhi - prm.zlo;
+    const int z0 = prm.zlo + (int)(((int64_t)span * chunk) / prm.nchunks);
+    const int z1 = prm.zlo + (int)(((int64_t)span * (chunk + 1)) / prm.nchunks);
+
+    if (tid == 0) {
+        for (int i = 0; i < C::NSP; ++i) { mbar_init(&fullP[i], 1); mbar_init(&emptyP[i], C::NWC); }
+        for (int i = 0; i < C::NSK; ++i) { mbar_init(&fullK[i], 1); mbar_init(&emptyK[i], C::NWC); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (z1 <= z0) return;
+
+    // Load l = 0 .. nload-1 brings p plane j = z0 - R + l (buffer plane j + R,
+    // halo'd x-y tile) into p slot l % NSP; for l >= 2R it also brings the
+    // p_prev and K tiles of plane z = j - R into (p_prev, K) slot (l-2R) % NSK.
+    // Slot release (consumers, one arrive per warp):
+    //   warm-up / tail planes (j < z0 or j >= z1): right after the column read;
+    //   planes z in [z0, z1): after their update at iteration z + R.
+    const int nload = (z1 - z0) + 2 * R;
+    if (warp == C::NWC) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            tma_prefetch_desc(&map_p); tma_prefetch_desc(&map_pp); tma_prefetch_desc(&map_k);
+            for (int l = 0; l < nload; ++l) {
+                const int j = z0 - R + l;
+                const int s = l % C::NSP;
+                mbar_wait(&emptyP[s], ((l / C::NSP) & 1) ^ 1);
+                mbar_expect_tx(&fullP[s], C::P_BYTES);
+#pragma unroll
+                for (int pc = 0; pc < C::NPP; ++pc)
+                    tma_load_3d(sP + s * C::P_FLOATS + pc * C::PPAD, &map_p, &fullP[s], x0 - 4 + pc * C::PBW,
+                                y0 - C::HY, j + R);
+                if (l >= 2 * R) {
+                    const int z = j - R, kl = l - 2 * R, ks = kl % C::NSK;
+                    mbar_wait(&emptyK[ks], ((kl / C::NSK) & 1) ^ 1);
+                    mbar_expect_tx(&fullK[ks], 2 * C::T_BYTES);
+                    float *dst = sK + ks * C::K_FLOATS;
+#pragma unroll
+                    for (int pc = 0; pc < C::NTP; ++pc) {
+                        tma_load_3d(dst + pc * C::TBW, &map_pp, &fullK[ks], x0 + pc * C::TBW, y0, z + R);
+                        tma_load_3d(dst + C::T_FLOATS + pc * C::TBW, &map_k, &fullK[ks], x0 + pc * C::TBW, y0, z);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int tx = tid % C::NTX, ty = tid / C::NTX;
+    const int xb = x0 + 4 * tx;                   // first of this thread's 4 x points
+    const int yb = y0 + ty * C::NY;               // first of its NY rows
+    const int64_t nx = prm.nx, ny = prm.ny;
+    const int cL = C::pcol(4 * tx), cM = C::pcol(4 * tx + 4), cR = C::pcol(4 * tx + 8);
+
+    bool inx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    bool iny[C::NY];
+#pragma unroll
+    for (int yy = 0; yy < C::NY; ++yy) iny[yy] = (C::NDIM == 3) && (yb + yy >= R) && (yb + yy < ny - R);
+
+    // sources that fall in this CTA's tile and chunk
+    uint32_t smask = 0;
+    for (int s = 0; s < prm.nsrc; ++s)
+        if (prm.sx[s] >= x0 && prm.sx[s] < x0 + C::TX && prm.sy[s] >= y0 && prm.sy[s] < y0 + C::TY &&
+            prm.sz[s] >= z0 && prm.sz[s] < z1)
+            smask |= 1u << s;
+    int rp = prm.rec.off ? prm.rec.off[unit] : 0;
+    const int rend = prm.rec.off ? prm.rec.off[unit + 1] : 0;
+    int rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
+
+    float4 q[2 * R + 1][C::NY];
+#pragma unroll
+    for (int i = 0; i < 2 * R + 1; ++i)
+#pragma unroll
+        for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    constexpr float c0 = tap(R, 0);
+
+    for (int l = 0; l < nload; ++l) {
+        const int j = z0 - R + l;
+        const int s = l % C::NSP;
+        mbar_wait(&fullP[s], (l / C::NSP) & 1);
+        const float *tp = sP + s * C::P_FLOATS;
+        // shift the register queue and append this thread's column of plane j
+#pragma unroll
+        for (int i = 0; i < 2 * R; ++i)
+#pragma unroll
+            for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = q[i + 1][yy];
+#pragma unroll
+        for (int yy = 0; yy < C::NY; ++yy)
+            q[2 * R][yy] = lds128(tp + (ty * C::NY + yy + C::HY) * C::BX + cM);
+        if (j < z0 || j >= z1) {               // z-taps only: slot free now
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyP[s]);
+        }
+        if (l < 2 * R) continue;
+
+        const int z = j - R;                       // plane computed now
+        const int sz_ = (l - R) % C::NSP;          // its p tile (x-y taps)
+        const float *tz = sP + sz_ * C::P_FLOATS;
+        const int kl = l - 2 * R, ks = kl % C::NSK;
+        mbar_wait(&fullK[ks], (kl / C::NSK) & 1);
+        const float *tk = sK + ks * C::K_FLOATS;
+        const int64_t gz = prm.gz0 + z;
+        const bool inz = (gz >= R) && (gz < prm.nzg - R);
+
+        float4 col[C::NY + 2 * C::HY];
+        if (C::NDIM == 3) {
+#pragma unroll
+            for (int i = 0; i < C::NY + 2 * C::HY; ++i)
+                col[i] = lds128(tz + (ty * C::NY + i) * C::BX + cM);
+        }
+        float4 out[C::NY];
+#pragma unroll
+        for (int yy = 0; yy < C::NY; ++yy) {
+            const float *row = tz + (ty * C::NY + yy + C::HY) * C::BX;
+            const float4 L4 = lds128(row + cL), M4 = q[R][yy], R4 = lds128(row + cR);
+            const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w,
+                                 R4.x, R4.y, R4.z, R4.w};
+            const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
+            const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float pc = a[4 + e];
+                float sx = __fmul_rn(c0, pc);
+#pragma unroll
+                for (int m = 1; m <= R; ++m)
+                    sx = __fmaf_rn(tap(R, m), __fadd_rn(a[4 + e - m], a[4 + e + m]), sx);
+                float S = inx[e] ? sx : 0.f;
+                if (C::NDIM == 3) {
+                    float sy = __fmul_rn(c0, pc);
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+                        sy = __fmaf_rn(tap(R, m),
+                                       __fadd_rn(f4(col[yy + C::HY - m], e), f4(col[yy + C::HY + m], e)), sy);
+                    S = iny[yy] ? __fadd_rn(S, sy) : S;
+                }
+                float szz = __fmul_rn(c0, pc);
+#pragma unroll
+                for (int m = 1; m <= R; ++m)
+                    szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(q[R - m][yy], e), f4(q[R + m][yy], e)), szz);
+                S = inz ? __fadd_rn(S, szz) : S;
+                const float upd = __fmaf_rn(f4(kk4, e), S, __fmaf_rn(2.f, pc, -f4(pp4, e)));
+                f4set(out[yy], e, upd);
+            }
+        }
+        // release the (p_prev, K) slot and the p slot of plane z (x-y taps done)
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&emptyK[ks]); mbar_arrive(&emptyP[sz_]); }
+
+        // receivers (raw P^{k+1}) -- before the injection
+        while (rnext_z == z) {
+            const int ry = prm.rec.y[rp], rx = prm.rec.x[rp];
+            const int dy = ry - yb, dx = rx - xb;
+            if (dy >= 0 && dy < C::NY && dx >= 0 && dx < 4) {
+#pragma unroll
+                for (int yy = 0; yy < C::NY; ++yy)
+                    if (yy == dy) prm.trace_row[prm.rec.id[rp]] = f4(out[yy], dx);
+            }
+            ++rp;
+            rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
+        }
+        // eager injection of w_{k+1} (registration order)
+        if (smask) {
+            for (int s2 = 0; s2 < prm.nsrc; ++s2) {
+                if (!((smask >> s2) & 1u) || prm.sz[s2] != z) continue;
+                const int dy = prm.sy[s2] - yb, dx = prm.sx[s2] - xb;
+                if (dy >= 0 && dy < C::NY && dx >= 0 && dx < 4) {
+#pragma unroll
+                    for (int yy = 0; yy < C::NY; ++yy)
+                        if (yy == dy) {
+                            const float v = f4(out[yy], dx);
+                            prm.src_raw[s2] = v;
+                            f4set(out[yy], dx, __fadd_rn(v, prm.w[s2]));
+                        }
+                }
+            }
+        }
+        // store p_next in place of p_prev (float4; rows outside the grid skipped)
+        if (xb < prm.pitch) {
+            float *dst = prm.pnext + ((int64_t)(z + R) * ny + yb) * prm.pitch + xb;
+#pragma unroll
+            for (int yy = 0; yy < C::NY; ++yy)
+                if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ naive kernels (B8)
+// One thread per point, global loads, the same canonical expression.  Debug /
+// reference path: three launches per step (stencil, receiver gather, injection).
+template <int R, int NDIM>
+__global__ void naive_step_kernel(const StepParams prm) {
+    const int64_t nx = prm.nx, ny = prm.ny, P = prm.pitch;
+    const int64_t npl = nx * ny;
+    const int64_t total = npl * (prm.zhi - prm.zlo);
+    constexpr float c0 = tap(R, 0);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = prm.zlo + t / npl;
+        const int64_t rem = t % npl;
+        const int64_t y = rem / nx, x = rem % nx;
+        const int64_t i = ((z + R) * ny + y) * P + x;     // index in a field buffer
+        const float pc = prm.p[i];
+        const int64_t gz = prm.gz0 + z;
+        float S = 0.f;
+        {
+            float s = __fmul_rn(c0, pc);
+            if (x >= R && x < nx - R) {
+#pragma unroll
+                for (int m = 1; m <= R; ++m) s = __fmaf_rn(tap(R, m), __fadd_rn(prm.p[i - m], prm.p[i + m]), s);
+                S = s;
+            }
+        }
+        if (NDIM == 3 && y >= R && y < ny - R) {
+            float s = __fmul_rn(c0, pc);
+#pragma unroll
+            for (int m = 1; m <= R; ++m)
+                s = __fmaf_rn(tap(R, m), __fadd_rn(prm.p[i - m * P], prm.p[i + m * P]), s);
+            S = __fadd_rn(S, s);
+        }
+        if (gz >= R && gz < prm.nzg - R) {
+            const int64_t pz = ny * P;
+            float s = __fmul_rn(c0, pc);
+#pragma unroll
+            for (int m = 1; m <= R; ++m)
+                s = __fmaf_rn(tap(R, m), __fadd_rn(prm.p[i - m * pz], prm.p[i + m * pz]), s);
+            S = __fadd_rn(S, s);
+        }
+        const int64_t ik = (z * ny + y) * P + x;
+        prm.pnext[i] = __fmaf_rn(prm.K[ik], S, __fmaf_rn(2.f, pc, -prm.pnext[i]));
+    }
+}
+
+// receivers of the naive path: trace_row[id] = p_next at (z, y, x) (raw, before injection)
+template <int R>
+__global__ void gather_receivers_kernel(const StepParams prm) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= prm.nrec_local) return;
+    const int64_t i = ((int64_t)(prm.rec.z[j] + R) * prm.ny + prm.rec.y[j]) * prm.pitch + prm.rec.x[j];
+    prm.trace_row[prm.rec.id[j]] = prm.pnext[i];
+}
+
+// add_source on a field buffer, registration order; records the raw values.
+// field = buffer base; sources with sz outside [0, nz) are skipped (other slab).
+template <int R>
+__global__ void inject_kernel(float *field, const StepParams prm) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int s = 0; s < prm.nsrc; ++s) {
+        if (prm.sz[s] < 0 || prm.sz[s] >= prm.nz) continue;
+        const int64_t i = ((int64_t)(prm.sz[s] + R) * prm.ny + prm.sy[s]) * prm.pitch + prm.sx[s];
+        const float v = field[i];
+        prm.src_raw[s] = v;
+        field[i] = __fadd_rn(v, prm.w[s]);
+    }
+}
+
+}  // namespace fdk

@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle.
+
+Every test follows the paper's five-step test procedure: inputs
+initialised on the host -> copied in by fd_create / fd_set_* -> the routine
+(fd_step) -> copied out (fd_get_*) -> asserted on the host.
+
+Tolerances: relative L2 <= 1e-4 for fp32 fields and
+traces vs fp64 (north star); bitwise for index/halo placement (light cone
+masks, band zeros, trace == wavefield sample, mirror symmetry, fused == naive).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2311_05038_b200.build import build_lib
+    build_lib()
+    import paper_2311_05038_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    import oracle as o
+    o.build()
+    return o
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return float(np.linalg.norm(a))
+    return float(np.linalg.norm(a - b) / nb)
+
+
+def run_gpu(fd, vel, h, dt, order, steps, sources, receivers, options=None, P0=None, Pm1=None):
+    with fd.Simulation(vel, h, dt, order, options=options) as sim:
+        if P0 is not None:
+            sim.set_wavefield(fd.FD_FIELD_CUR, P0)
+        if Pm1 is not None:
+            sim.set_wavefield(fd.FD_FIELD_PREV, Pm1)
+        for (idx, f, t0, amp) in sources:
+            sim.add_source(idx, f, t0, amp)
+        if receivers:
+            sim.set_receivers(receivers)
+        sim.step(steps)
+        P = sim.wavefield(fd.FD_FIELD_CUR)
+        Pp = sim.wavefield(fd.FD_FIELD_PREV)
+        T = sim.traces() if receivers else None
+        info = sim.info()
+    return P, Pp, T, info
+
+
+def _rand_vel(dims, seed=0, lo=1500.0, hi=2500.0):
+    return np.random.default_rng(seed).uniform(lo, hi, dims).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# Parity vs the oracle on ragged sizes spanning several tiles
+# ---------------------------------------------------------------------------
+CASES = [
+    # dims, order, steps
+    ((37, 45, 70), 2, 40),
+    ((33, 70, 131), 4, 30),
+    ((29, 40, 66), 6, 25),
+    ((40, 36, 140), 8, 30),
+    ((90, 300), 2, 150),
+    ((61, 600), 4, 120),
+    ((75, 1100), 8, 100),
+    ((45, 257), 6, 90),
+]
+
+
+@pytest.mark.parametrize("dims,order,steps", CASES)
+@pytest.mark.parametrize("kernel", [2, 1])
+def test_parity_vs_oracle(fd, oracle, dims, order, steps, kernel):
+    vel = _rand_vel(dims, seed=len(dims) + order)
+    h = 10.0
+    dt = 0.6 * oracle.cfl_max(len(dims), order) * h / float(vel.max())
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.03, 1.0),
+           (tuple([dims[0] // 3] + [d // 3 + 1 for d in dims[1:]]), 18.0, 0.04, -0.5)]
+    recs = [tuple([dims[0] // 2 + 2] + [d // 2 - 3 for d in dims[1:]]), tuple(d // 2 for d in dims),
+            tuple([0] * len(dims)), tuple([order // 2] * len(dims))]
+    P, Pp, T, info = run_gpu(fd, vel, h, dt, order, steps, src, recs, options={fd.FD_OPT_KERNEL: kernel})
+    Po, Ppo, To = oracle.run(vel, h, dt, order, steps, src, recs, nthreads=4)
+    assert info["kernel"] == kernel
+    assert rel_l2(P, Po) <= TOL
+    assert rel_l2(Pp, Ppo) <= TOL
+    assert rel_l2(T, To) <= TOL
+    # receivers in the band read exactly 0 (R#3, R#6)
+    assert np.all(T[2] == 0.0)
+
+
+@pytest.mark.parametrize("dims,order", [((41, 37, 150), 2), ((35, 70, 100), 8), ((80, 700), 4)])
+def test_fused_equals_naive_bitwise_all_tiles(fd, dims, order):
+    vel = _rand_vel(dims, seed=3)
+    h, dt = 10.0, 0.5e-3
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0), (tuple(d // 2 for d in dims), 10.0, 0.03, 2.0)]
+    recs = [tuple(d // 2 for d in dims), tuple([d // 4 for d in dims])]
+    ref = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_KERNEL: 1})
+    from paper_2311_05038_b200 import fd as fdm
+    ntiles = 0
+    for t in range(64):
+        try:
+            opts = {fd.FD_OPT_KERNEL: 2, fd.FD_OPT_TILE: t}
+            got = run_gpu(fd, vel, h, dt, order, 37, src, recs, options=opts)
+        except fdm.FDError:
+            continue
+        ntiles += 1
+        for a, b in zip(got[:3], ref[:3]):
+            assert np.array_equal(a, b), (t, got[3])
+        for zc in (1, 3):
+            got = run_gpu(fd, vel, h, dt, order, 37, src, recs,
+                          options={fd.FD_OPT_KERNEL: 2, fd.FD_OPT_TILE: t, fd.FD_OPT_ZCHUNKS: zc})
+            for a, b in zip(got[:3], ref[:3]):
+                assert np.array_equal(a, b), (t, zc)
+    assert ntiles >= 3
+
+
+# ---------------------------------------------------------------------------
+# Bit-exact contracts: indexing, band, traces, symmetry, light cone
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("ndim,order", [(2, 2), (2, 8), (3, 2), (3, 4), (3, 8)])
+def test_light_cone_mask_matches_oracle(fd, oracle, ndim, order):
+    """After j steps from a point source, the nonzero mask of the fp32 field is
+    the oracle's (equal for j <= 8): any misplaced tap, index or halo plane
+    creates a nonzero outside it."""
+    n = 61 if ndim == 2 else 31
+    dims = (n,) * ndim
+    vel = _rand_vel(dims, seed=5, lo=1800, hi=2200)
+    s = tuple([n // 2 - 2] + [n // 2 + 1] * (ndim - 1))
+    src = [(s, 25.0, 0.0, 1.0)]
+    for j in (1, 2, 5, 8):
+        P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, j, src, [])
+        Po, Ppo, _ = oracle.run(vel, 10.0, 1e-3, order, j, src)
+        assert np.array_equal(P != 0, Po != 0), j
+        assert np.array_equal(Pp != 0, Ppo != 0), j
+        if j == 1:
+            assert np.count_nonzero(P) == 1 + 2 * ndim * (order // 2)
+
+
+@pytest.mark.parametrize("kernel", [2, 1])
+def test_traces_equal_wavefield_samples_bitwise(fd, kernel):
+    dims = (30, 34, 70)
+    vel = _rand_vel(dims, seed=9)
+    src = [((15, 17, 35), 25.0, 0.02, 1.0)]
+    recs = [(15, 17, 35), (15, 17, 38), (20, 5, 60), (1, 1, 1)]
+    steps = 12
+    _, _, T, _ = run_gpu(fd, vel, 10.0, 1e-3, 4, steps, src, recs, options={fd.FD_OPT_KERNEL: kernel})
+    for k in range(steps):
+        P, _, _, _ = run_gpu(fd, vel, 10.0, 1e-3, 4, k + 1, src, [], options={fd.FD_OPT_KERNEL: kernel})
+        for j, q in enumerate(recs):
+            assert T[j, k] == P[q], (k, j)
+
+
+def test_incremental_steps_equal_one_call(fd):
+    dims = (26, 40, 90)
+    vel = _rand_vel(dims, seed=11)
+    src = [((13, 20, 45), 25.0, 0.02, 1.0)]
+    recs = [(13, 20, 50)]
+    P1, Pp1, T1, _ = run_gpu(fd, vel, 10.0, 1e-3, 8, 30, src, recs)
+    with fd.Simulation(vel, 10.0, 1e-3, 8) as sim:
+        sim.add_source(*src[0])
+        sim.set_receivers(recs)
+        for n in (1, 0, 7, 22):
+            sim.step(n)
+        P2, Pp2, T2 = sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces()
+    assert np.array_equal(P1, P2) and np.array_equal(Pp1, Pp2) and np.array_equal(T1, T2)
+
+
+@pytest.mark.parametrize("ndim,order", [(2, 2), (2, 8), (3, 2), (3, 8)])
+def test_band_exactly_zero_and_mirror_symmetry(fd, ndim, order):
+    n = 65 if ndim == 2 else 33
+    dims = (n,) * ndim
+    vel = np.full(dims, 2000.0, np.float32)
+    c = tuple([n // 2] * ndim)
+    P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, 60, [(c, 25.0, 0.04, 1.0)], [])
+    r = order // 2
+    for X in (P, Pp):
+        for ax in range(ndim):
+            idx = [slice(None)] * ndim
+            idx[ax] = slice(0, r)
+            assert np.all(X[tuple(idx)] == 0.0)
+            idx[ax] = slice(n - r, n)
+            assert np.all(X[tuple(idx)] == 0.0)
+            assert np.array_equal(X, np.flip(X, axis=ax))
+        assert np.array_equal(X, np.swapaxes(X, ndim - 2, ndim - 1))
+
+
+def test_one_step_closed_form_fp32(fd, oracle):
+    """S:361 one-step closed form, evaluated in fp32 in the canonical order."""
+    for ndim in (2, 3):
+        for order in (2, 4, 6, 8):
+            r = order // 2
+            n = 4 * r + 1
+            dims = (n,) * ndim
+            v, h, dt, f, t0, amp = 2500.0, 10.0, 1e-3, 20.0, 0.03, 1.7
+            s = (2 * r,) * ndim
+            P, Pp, _, _ = run_gpu(fd, np.full(dims, v, np.float32), h, dt, order, 1, [(s, f, t0, amp)], [])
+            Po, _, _ = oracle.run(np.full(dims, v), h, dt, order, 1, [(s, f, t0, amp)])
+            assert np.count_nonzero(P) == 1 + 2 * ndim * r
+            assert np.array_equal(P != 0, Po != 0)
+            assert rel_l2(P, Po) < 1e-6
+
+
+def test_source_and_receiver_edge_cases(fd, oracle):
+    """Source in the band (literal rule), a receiver on the source (pre-injection
+    value), two sources at one point (registration order), zero source."""
+    dims = (24, 30, 40)
+    vel = _rand_vel(dims, seed=13)
+    src = [((1, 15, 20), 25.0, 0.02, 1.0), ((12, 15, 20), 25.0, 0.02, 1.0), ((12, 15, 20), 12.0, 0.03, -0.7),
+           ((5, 5, 5), 25.0, 0.02, 0.0)]
+    recs = [(12, 15, 20), (1, 15, 20), (12, 15, 22)]
+    for kernel in (1, 2):
+        P, Pp, T, _ = run_gpu(fd, vel, 10.0, 1e-3, 4, 40, src, recs, options={fd.FD_OPT_KERNEL: kernel})
+        Po, Ppo, To = oracle.run(vel, 10.0, 1e-3, 4, 40, src, recs)
+        assert rel_l2(P, Po) <= TOL and rel_l2(Pp, Ppo) <= TOL and rel_l2(T, To) <= TOL
+
+
+def test_initial_fields_standing_wave(fd, oracle):
+    """fd_set_wavefield hook: the exact discrete standing wave (r=1), fp32."""
+    n = 65
+    dims = (n, n)
+    h, v = 10.0, 1500.0
+    dt = 0.5 * oracle.cfl_max(2, 2) * h / v
+    Z, X = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    L = (n - 1) * h
+    mode = np.sin(np.pi * 2 * X * h / L) * np.sin(np.pi * 3 * Z * h / L)
+    C = v * dt / h
+    wd = 2 * np.arcsin(C * np.sqrt(np.sin(np.pi * 2 / L * h / 2) ** 2 + np.sin(np.pi * 3 / L * h / 2) ** 2))
+    P, _, _, _ = run_gpu(fd, np.full(dims, v, np.float32), h, dt, 2, 200, [], [],
+                         P0=mode.astype(np.float32), Pm1=(mode * np.cos(-wd)).astype(np.float32))
+    Po, _, _ = oracle.run(np.full(dims, v), h, dt, 2, 200, P0=mode.astype(np.float32).astype(np.float64),
+                          Pm1=(mode * np.cos(-wd)).astype(np.float32).astype(np.float64))
+    assert rel_l2(P, Po) <= TOL
+
+
+def test_state_errors(fd):
+    vel = np.full((20, 22), 2000.0, np.float32)
+    sim = fd.Simulation(vel, 10.0, 1e-3, 2)
+    with pytest.raises(fd.FDError) as e:
+        sim.add_source((30, 3), 10.0, 0.0)
+    assert e.value.status == -2
+    with pytest.raises(fd.FDError) as e:
+        sim.traces()
+    assert e.value.status == -7
+    sim.add_source((10, 11), 10.0, 0.0)
+    sim.step(2)
+    with pytest.raises(fd.FDError) as e:
+        sim.add_source((10, 11), 10.0, 0.0)
+    assert e.value.status == -7
+    with pytest.raises(fd.FDError) as e:
+        sim.set_receivers([(1, 1)])
+    assert e.value.status == -7
+    with pytest.raises(fd.FDError) as e:
+        sim.set_wavefield(fd.FD_FIELD_CUR, np.zeros((20, 22), np.float32))
+    assert e.value.status == -7
+    with pytest.raises(fd.FDError):
+        sim.step(-1)
+    sim.close()
+
+
+def test_torch_allocator_and_stream(fd):
+    import torch
+    from paper_2311_05038_b200 import fd as fdm
+    dims = (20, 30, 40)
+    vel = _rand_vel(dims, seed=17)
+    ref = run_gpu(fd, vel, 10.0, 1e-3, 2, 10, [((10, 15, 20), 25.0, 0.02, 1.0)], [(10, 15, 22)])
+    fdm.fd_set_allocator_torch()
+    try:
+        before = torch.cuda.memory_allocated()
+        s = torch.cuda.Stream()
+        with fd.Simulation(vel, 10.0, 1e-3, 2, stream=s.cuda_stream) as sim:
+            assert torch.cuda.memory_allocated() > before
+            sim.add_source((10, 15, 20), 25.0, 0.02, 1.0)
+            sim.set_receivers([(10, 15, 22)])
+            sim.step(10)
+            got = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
+    finally:
+        fdm.fd_reset_allocator()
+    for a, b in zip(got, ref[:3]):
+        assert np.array_equal(a, b)
