@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -135,6 +136,52 @@ static const std::vector<TileCfg> &tile_table() {
 }
 
 // ------------------------------------------------------------------ context
+// ------------------------------------------------------------------ NCCL (dlopen)
+// NCCL is loaded at run time (libnccl.so.2: torch's bundled copy when torch has
+// loaded it, else the system one) so the library loads on machines without it.
+typedef void *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclFloat32 = 7 };
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+#define NCCL_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+            NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+            NCCL_SYM(CommInitRank, "ncclCommInitRank");
+            NCCL_SYM(CommDestroy, "ncclCommDestroy");
+            NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+            NCCL_SYM(Send, "ncclSend");
+            NCCL_SYM(Recv, "ncclRecv");
+            NCCL_SYM(GroupStart, "ncclGroupStart");
+            NCCL_SYM(GroupEnd, "ncclGroupEnd");
+            NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef NCCL_SYM
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+                     api.GroupStart && api.GroupEnd && api.GetErrorString;
+        }
+    }
+    return api;
+}
+
+// ------------------------------------------------------------------ context
 struct SourceDef {
     int64_t g[3];     // global (z, y, x)
     double f, t0, amp;
@@ -143,41 +190,62 @@ struct RecDef {
     int64_t g[3];
 };
 
+// One kernel launch per step over local planes [zlo, zhi) of a slab.
+struct Region {
+    int32_t zlo = 0, zhi = 0;
+    int zchunks = 1;
+    int ctas = 0;
+    bool boundary = false;      // launched on the comm stream before the exchange
+    int32_t *d_rec = nullptr;   // [4 * nrec + units + 1]: z, y, x, id, CSR offsets
+    int nrec = 0;
+};
+
+// A z-slab [z0, z1) of the global grid with its own buffers (halo planes r on
+// each side).  One per context, except FD_OPT_VSLABS (several on one GPU).
+struct Slab {
+    int64_t z0 = 0, z1 = 0, nz = 0;
+    float *A = nullptr, *B = nullptr, *K = nullptr;
+    float *d_src_raw = nullptr;
+    CUtensorMap mA_halo, mB_halo, mA_tile, mB_tile, mK;
+    std::vector<Region> regions;
+};
+
 struct fd_ctx {
     int ndim = 0, order = 0, R = 0;
     double h = 0, dt = 0;
     int64_t nxg = 0, nyg = 0, nzg = 0;    // global extents (ny = 1 in 2D)
-    int64_t nz = 0, z0 = 0, z1 = 0;       // local planes [z0, z1)
+    int64_t z0 = 0, z1 = 0;               // planes owned by this context
     int64_t pitch = 0;
     int rank = 0, nranks = 1, device = 0;
     bool poisoned = false;
     bool started = false;
-    bool injected = false;                // w_k already injected into the CUR buffer
+    bool injected = false;                // w_k already injected into the CUR buffers
     int64_t k = 0;                        // steps done
     int64_t launches = 0;
-    cudaStream_t stream = nullptr;
-    float *A = nullptr, *B = nullptr, *K = nullptr;   // A = current p after even #steps
+    cudaStream_t stream = nullptr;        // user stream (interior kernels)
+    cudaStream_t comm_stream = nullptr;   // boundary kernels + NCCL (distributed)
+    cudaEvent_t ev_step = nullptr, ev_comm = nullptr;
     bool cur_is_A = true;
     std::vector<SourceDef> src;
     std::vector<RecDef> rec;
-    // device-side receiver tables
-    int32_t *d_rec = nullptr;             // [5 * nrec_local + nunits + 1]
-    int nrec_local = 0;
+    std::vector<Slab> slabs;
+    std::vector<float> vel_host;          // kept until the slabs are built (VSLABS)
     float *d_traces = nullptr;            // step-major [trace_cap][nrec]
     int64_t trace_cap = 0;
-    float *d_src_raw = nullptr;
-    std::vector<float> h_src_raw;
+    // distributed
+    ncclComm_t comm = nullptr;
+    ncclUniqueId nccl_id;
+    bool have_id = false;
     // kernel configuration
     int opt_kernel = 0, opt_tile = -1, opt_zchunks = 0, opt_async = 0, opt_graph = 1, opt_vslabs = 1;
-    int tile = -1, zchunks = 1, ctas = 0;
-    CUtensorMap mapA_halo, mapB_halo, mapA_tile, mapB_tile, mapK;
-    bool maps_ready = false;
+    int tile = -1, occ = 0, nsm = 148;
     double dev_bytes = 0;
 };
 
-static inline int64_t buf_floats(const fd_ctx *c) { return (c->nz + 2 * c->R) * c->nyg * c->pitch; }
-static inline float *cur_buf(fd_ctx *c) { return c->cur_is_A ? c->A : c->B; }
-static inline float *prev_buf(fd_ctx *c) { return c->cur_is_A ? c->B : c->A; }
+static inline int64_t plane_floats(const fd_ctx *c) { return c->nyg * c->pitch; }
+static inline int64_t buf_floats(const fd_ctx *c, const Slab &s) { return (s.nz + 2 * c->R) * plane_floats(c); }
+static inline float *cur_buf(const fd_ctx *c, const Slab &s) { return c->cur_is_A ? s.A : s.B; }
+static inline float *prev_buf(const fd_ctx *c, const Slab &s) { return c->cur_is_A ? s.B : s.A; }
 
 static double scale_of(int R) { return tap_scale(R); }
 
@@ -207,15 +275,71 @@ static fd_status partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_
     return FD_OK;
 }
 
-static void destroy_buffers(fd_ctx *c) {
-    dev_free(c->A); dev_free(c->B); dev_free(c->K);
-    dev_free(c->d_rec); dev_free(c->d_traces); dev_free(c->d_src_raw);
-    c->A = c->B = c->K = nullptr;
-    c->d_rec = nullptr; c->d_traces = nullptr; c->d_src_raw = nullptr;
+static void free_slab(Slab &s) {
+    dev_free(s.A); dev_free(s.B); dev_free(s.K); dev_free(s.d_src_raw);
+    s.A = s.B = s.K = s.d_src_raw = nullptr;
+    for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
+}
+
+static void destroy_all(fd_ctx *c) {
+    for (auto &s : c->slabs) free_slab(s);
+    dev_free(c->d_traces);
+    c->d_traces = nullptr;
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    c->comm = nullptr;
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_step) cudaEventDestroy(c->ev_step);
+    if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    c->comm_stream = nullptr; c->ev_step = c->ev_comm = nullptr;
+}
+
+// K = (v dt / h)^2 / scale in fp64, rounded once (R#7), into a pitched host
+// array; threads split the planes (host-side setup, off the step path).
+static void compute_K(const fd_ctx *c, const float *v, int64_t nz, std::vector<float> &Kh) {
+    Kh.assign((size_t)(nz * c->nyg * c->pitch), 0.f);
+    const double sc = scale_of(c->R), dt = c->dt, h = c->h;
+    const int64_t nyg = c->nyg, nxg = c->nxg, pitch = c->pitch;
+    auto work = [&](int64_t za, int64_t zb) {
+        for (int64_t z = za; z < zb; ++z)
+            for (int64_t y = 0; y < nyg; ++y) {
+                const float *vr = v + (z * nyg + y) * nxg;
+                float *kr = Kh.data() + (z * nyg + y) * pitch;
+                for (int64_t x = 0; x < nxg; ++x) {
+                    const double cv = (double)vr[x] * dt / h;
+                    kr[x] = (float)(cv * cv / sc);
+                }
+            }
+    };
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, nz));
+    nt = std::min(nt, 32);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work, nz * t / nt, nz * (t + 1) / nt);
+    for (auto &t : th) t.join();
+}
+
+// Allocate a slab's buffers and upload its K (v holds the slab's planes).
+static fd_status build_slab(fd_ctx *c, Slab &s, const float *v) {
+    const size_t fbytes = (size_t)buf_floats(c, s) * 4;
+    const size_t kbytes = (size_t)(s.nz * plane_floats(c)) * 4;
+    s.A = (float *)dev_alloc(fbytes);
+    s.B = (float *)dev_alloc(fbytes);
+    s.K = (float *)dev_alloc(kbytes);
+    s.d_src_raw = (float *)dev_alloc(kMaxSources * 4);
+    if (!s.A || !s.B || !s.K || !s.d_src_raw)
+        return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
+    c->dev_bytes += 2.0 * fbytes + kbytes;
+    std::vector<float> Kh;
+    compute_K(c, v, s.nz, Kh);
+    CUDA_TRY(c, cudaMemcpy(s.K, Kh.data(), kbytes, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemset(s.A, 0, fbytes));
+    CUDA_TRY(c, cudaMemset(s.B, 0, fbytes));
+    CUDA_TRY(c, cudaMemset(s.d_src_raw, 0, kMaxSources * 4));
+    return FD_OK;
 }
 
 static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double h, double dt, int order,
-                             const float *vel, uint32_t flags, int rank, int nranks, int device, int vel_is_slab) {
+                             const float *vel, uint32_t flags, int rank, int nranks, int device, int vel_is_slab,
+                             const void *nccl_id) {
     if (!out) return fail(FD_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (ndim != 2 && ndim != 3) return fail(FD_ERR_ARG, "ndim must be 2 or 3 (got %d)", ndim);
@@ -235,7 +359,9 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     if (nranks > 1 || rank != 0) {
         fd_status s = partition(nzg, nranks, rank, &z0, &z1);
         if (s) return s;
-        if (z1 - z0 < R) return fail(FD_ERR_ARG, "slab of %lld planes thinner than r=%d", (long long)(z1 - z0), R);
+        if (nranks > 1 && z1 - z0 < 2 * R)
+            return fail(FD_ERR_ARG, "slab of %lld planes thinner than 2r=%d", (long long)(z1 - z0), 2 * R);
+        if (nranks > 1 && !nccl_id) return fail(FD_ERR_ARG, "nccl_id is NULL with nranks > 1");
     }
     const int64_t nz = z1 - z0;
     const int64_t plane = nyg * nxg;
@@ -253,6 +379,7 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     if (!(flags & FD_FLAG_ALLOW_UNSTABLE) && ratio > lim)
         return fail(FD_ERR_UNSTABLE, "unstable: max(v)*dt/h = %.6f exceeds the CFL limit %.6f (ratio %.4f)", ratio,
                     lim, ratio / lim);
+    if (nranks > 1 && !nccl().ok) return fail(FD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -265,43 +392,29 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     }
     fd_ctx *c = new fd_ctx();
     c->ndim = ndim; c->order = order; c->R = R; c->h = h; c->dt = dt;
-    c->nxg = nxg; c->nyg = nyg; c->nzg = nzg; c->z0 = z0; c->z1 = z1; c->nz = nz;
+    c->nxg = nxg; c->nyg = nyg; c->nzg = nzg; c->z0 = z0; c->z1 = z1;
     c->rank = rank; c->nranks = nranks;
     cudaGetDevice(&c->device);
+    cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
     c->pitch = (nxg + 31) / 32 * 32;
-    const size_t fbytes = (size_t)buf_floats(c) * 4;
-    const size_t kbytes = (size_t)(nz * nyg * c->pitch) * 4;
-    c->A = (float *)dev_alloc(fbytes);
-    c->B = (float *)dev_alloc(fbytes);
-    c->K = (float *)dev_alloc(kbytes);
-    c->d_src_raw = (float *)dev_alloc(kMaxSources * 4);
-    if (!c->A || !c->B || !c->K || !c->d_src_raw) {
-        destroy_buffers(c);
-        delete c;
-        return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
+    if (nranks > 1) {
+        memcpy(&c->nccl_id, nccl_id, sizeof(ncclUniqueId));
+        c->have_id = true;
     }
-    c->dev_bytes = 2.0 * fbytes + kbytes;
-    // K = (v dt / h)^2 / scale in fp64, rounded once (R#7), padded rows zero
-    std::vector<float> Kh((size_t)(nz * nyg * c->pitch), 0.f);
-    const double sc = scale_of(R);
-    for (int64_t z = 0; z < nz; ++z)
-        for (int64_t y = 0; y < nyg; ++y) {
-            const float *vr = vloc + (z * nyg + y) * nxg;
-            float *kr = Kh.data() + (z * nyg + y) * c->pitch;
-            for (int64_t x = 0; x < nxg; ++x) {
-                const double cv = (double)vr[x] * dt / h;
-                kr[x] = (float)(cv * cv / sc);
-            }
-        }
-    cudaError_t e = cudaMemcpy(c->K, Kh.data(), kbytes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(c->A, 0, fbytes);
-    if (e == cudaSuccess) e = cudaMemset(c->B, 0, fbytes);
-    if (e == cudaSuccess) e = cudaMemset(c->d_src_raw, 0, kMaxSources * 4);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) {
-        destroy_buffers(c);
+    // one slab now; FD_OPT_VSLABS re-splits before the first step (keeps the model)
+    c->slabs.resize(1);
+    Slab &s = c->slabs[0];
+    s.z0 = z0; s.z1 = z1; s.nz = nz;
+    fd_status st = build_slab(c, s, vloc);
+    if (st == FD_OK && nranks == 1) c->vel_host.assign(vloc, vloc + nloc);
+    if (st == FD_OK) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) st = fail(FD_ERR_CUDA, "device setup failed: %s", cudaGetErrorString(e));
+    }
+    if (st != FD_OK) {
+        destroy_all(c);
         delete c;
-        return fail(FD_ERR_CUDA, "device setup failed: %s", cudaGetErrorString(e));
+        return st;
     }
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -322,84 +435,85 @@ static int occupancy(const TileCfg &t) {
     return n;
 }
 
-// Pick the tile and z-chunk count: prefer one full wave of co-resident CTAs
-// (chunk-major order keeps neighbours in step for L2 halo reuse), then the
-// smallest halo re-read factor.
-static void choose_config(fd_ctx *c, int64_t span) {
+static int64_t ntiles_of(const fd_ctx *c, const TileCfg &t) {
+    return ((c->nxg + t.tx - 1) / t.tx) * ((c->nyg + t.ty - 1) / t.ty);
+}
+
+// z-chunks for a span of planes: fill one wave of resident CTAs (chunk-major
+// order keeps neighbours in step for L2 halo reuse), chunks >= max(4r, 8) planes.
+static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
+    if (c->opt_zchunks > 0) return (int)std::min<int64_t>(c->opt_zchunks, std::max<int64_t>(1, span));
+    const int64_t slots = (int64_t)c->nsm * occ, ntiles = ntiles_of(c, t);
+    int64_t ch = std::max<int64_t>(1, slots / ntiles);
+    ch = std::min<int64_t>(ch, std::max<int64_t>(1, span / std::max(4 * c->R, 8)));
+    return (int)ch;
+}
+
+// Pick the tile: maximise (wave fill) x (16 B / modelled bytes per point, with
+// the halo re-read and chunk warm-up planes counted).
+static void choose_tile(fd_ctx *c, int64_t span) {
     const auto &tab = tile_table();
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
     double best = -1;
-    int bi = -1, bchunks = 1;
+    int bi = -1, bocc = 0;
     for (int i = 0; i < (int)tab.size(); ++i) {
         const TileCfg &t = tab[i];
         if (t.ndim != c->ndim || t.r != c->R) continue;
         if (c->opt_tile >= 0 && i != c->opt_tile) continue;
         const int occ = occupancy(t);
         if (occ <= 0) continue;
-        const int64_t slots = (int64_t)nsm * occ;
-        const int64_t ntiles = ((c->nxg + t.tx - 1) / t.tx) * ((c->nyg + t.ty - 1) / t.ty);
-        int64_t chunks = c->opt_zchunks > 0 ? c->opt_zchunks : std::max<int64_t>(1, slots / ntiles);
-        chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, span / std::max(4 * c->R, 8)));
-        const int64_t units = ntiles * chunks;
+        const int64_t slots = (int64_t)c->nsm * occ;
+        const int64_t chunks = chunks_for(c, t, occ, span);
+        const int64_t units = ntiles_of(c, t) * chunks;
         const int64_t waves = (units + slots - 1) / slots;
         const double fill = (double)units / (double)(waves * slots);
         const double halo = (double)(t.tx + 8) * (t.ty + (c->ndim == 3 ? 2 * c->R : 0)) / ((double)t.tx * t.ty);
         const double warm = (double)(2 * c->R * chunks) / (double)span;
         const double bytes = 12.0 + 4.0 * (halo + warm);
         const double score = fill * 16.0 / bytes;
-        if (score > best) { best = score; bi = i; bchunks = (int)chunks; }
+        if (score > best) { best = score; bi = i; bocc = occ; }
     }
     c->tile = bi;
-    c->zchunks = bchunks;
+    c->occ = bocc;
 }
 
-static fd_status prepare(fd_ctx *c) {
-    if (c->maps_ready) return FD_OK;
-    if (c->opt_kernel == 1) { c->maps_ready = true; return FD_OK; }
-    choose_config(c, c->nz);
-    if (c->tile < 0) return fail(FD_ERR_CUDA, "no fused kernel configuration fits this device");
+static fd_status make_maps(fd_ctx *c, Slab &s) {
     const TileCfg &t = tile_table()[c->tile];
-    const int64_t planes = c->nz + 2 * c->R;
+    const int64_t planes = s.nz + 2 * c->R;
     const int hy = c->ndim == 3 ? c->R : 0;
-    bool ok = make_map(&c->mapA_halo, c->A, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
-              make_map(&c->mapB_halo, c->B, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
-              make_map(&c->mapA_tile, c->A, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
-              make_map(&c->mapB_tile, c->B, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
-              make_map(&c->mapK, c->K, c->nxg, c->nyg, c->nz, c->pitch, t.tbw, t.ty);
+    bool ok = make_map(&s.mA_halo, s.A, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
+              make_map(&s.mB_halo, s.B, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
+              make_map(&s.mA_tile, s.A, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
+              make_map(&s.mB_tile, s.B, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
+              make_map(&s.mK, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, t.ty);
     if (!ok) {
         c->poisoned = true;
         return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     }
-    CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
-    c->maps_ready = true;
     return FD_OK;
 }
 
-// Build device receiver tables: local receivers sorted by (work unit, z), CSR
-// offsets per unit (fused) -- or a flat list (naive).
-static fd_status upload_receivers(fd_ctx *c) {
-    dev_free(c->d_rec);
-    c->d_rec = nullptr;
+// Receivers of a region, sorted by (work unit, z) with CSR offsets per unit
+// (fused kernel) -- or a flat list (naive kernel).
+static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g) {
+    dev_free(g.d_rec);
+    g.d_rec = nullptr;
     struct L { int32_t unit, z, y, x, id; };
     std::vector<L> loc;
-    int ntx = 1, nty = 1, ntiles = 1;
-    const TileCfg *t = c->tile >= 0 ? &tile_table()[c->tile] : nullptr;
+    const TileCfg *t = (c->opt_kernel == 1) ? nullptr : &tile_table()[c->tile];
+    int ntx = 1, ntiles = 1;
     if (t) {
         ntx = (int)((c->nxg + t->tx - 1) / t->tx);
-        nty = (int)((c->nyg + t->ty - 1) / t->ty);
-        ntiles = ntx * nty;
+        ntiles = (int)ntiles_of(c, *t);
     }
+    const int64_t span = g.zhi - g.zlo;
     for (size_t j = 0; j < c->rec.size(); ++j) {
-        const int64_t gz = c->rec[j].g[0];
-        if (gz < c->z0 || gz >= c->z1) continue;
-        L l{0, (int32_t)(gz - c->z0), (int32_t)c->rec[j].g[1], (int32_t)c->rec[j].g[2], (int32_t)j};
+        const int64_t lz = c->rec[j].g[0] - s.z0;
+        if (lz < g.zlo || lz >= g.zhi) continue;
+        L l{0, (int32_t)lz, (int32_t)c->rec[j].g[1], (int32_t)c->rec[j].g[2], (int32_t)j};
         if (t) {
-            const int64_t span = c->nz;
             int ch = 0;
-            // chunk containing plane z: the largest ch with floor(span*ch/nchunks) <= z
-            for (int q = 0; q < c->zchunks; ++q)
-                if ((span * q) / c->zchunks <= l.z) ch = q;
+            for (int q = 0; q < g.zchunks; ++q)
+                if (g.zlo + (span * q) / g.zchunks <= lz) ch = q;
             l.unit = ch * ntiles + (l.y / t->ty) * ntx + (l.x / t->tx);
         }
         loc.push_back(l);
@@ -407,10 +521,10 @@ static fd_status upload_receivers(fd_ctx *c) {
     std::stable_sort(loc.begin(), loc.end(), [](const L &a, const L &b) {
         return a.unit != b.unit ? a.unit < b.unit : a.z < b.z;
     });
-    const int nunits = t ? ntiles * c->zchunks : 0;
+    const int nunits = t ? ntiles * g.zchunks : 0;
     const int n = (int)loc.size();
-    c->nrec_local = n;
-    std::vector<int32_t> h((size_t)5 * n + nunits + 1, 0);
+    g.nrec = n;
+    std::vector<int32_t> h((size_t)4 * n + nunits + 1, 0);
     for (int i = 0; i < n; ++i) {
         h[i] = loc[i].z; h[n + i] = loc[i].y; h[2 * n + i] = loc[i].x; h[3 * n + i] = loc[i].id;
     }
@@ -419,9 +533,96 @@ static fd_status upload_receivers(fd_ctx *c) {
         while (i < n && loc[i].unit < u) ++i;
         off[u] = i;
     }
-    c->d_rec = (int32_t *)dev_alloc(h.size() * 4);
-    if (!c->d_rec) return fail(FD_ERR_NOMEM, "receiver table allocation failed");
-    CUDA_TRY(c, cudaMemcpy(c->d_rec, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    g.d_rec = (int32_t *)dev_alloc(h.size() * 4);
+    if (!g.d_rec) return fail(FD_ERR_NOMEM, "receiver table allocation failed");
+    CUDA_TRY(c, cudaMemcpy(g.d_rec, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    return FD_OK;
+}
+
+// Re-split the single slab into n virtual slabs on this GPU (FD_OPT_VSLABS).
+static fd_status split_virtual(fd_ctx *c, int n) {
+    if (n <= 1) return FD_OK;
+    if (c->nranks > 1) return fail(FD_ERR_STATE, "FD_OPT_VSLABS is for single-process contexts");
+    const int64_t nz = c->z1 - c->z0;
+    if (nz < (int64_t)n * 2 * c->R) return fail(FD_ERR_ARG, "too many virtual slabs for nz=%lld", (long long)nz);
+    // keep the current fields (fd_set_wavefield may have set them)
+    const int64_t pf = plane_floats(c);
+    std::vector<float> hA((size_t)(nz * pf)), hB((size_t)(nz * pf)), raw(kMaxSources);
+    Slab &o = c->slabs[0];
+    CUDA_TRY(c, cudaMemcpy(hA.data(), o.A + c->R * pf, hA.size() * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(hB.data(), o.B + c->R * pf, hB.size() * 4, cudaMemcpyDeviceToHost));
+    c->dev_bytes = 0;
+    free_slab(o);
+    c->slabs.assign(n, Slab());
+    const int64_t plane = c->nyg * c->nxg;
+    for (int q = 0; q < n; ++q) {
+        Slab &s = c->slabs[q];
+        int64_t a, b;
+        partition(nz, n, q, &a, &b);
+        s.z0 = c->z0 + a; s.z1 = c->z0 + b; s.nz = b - a;
+        fd_status st = build_slab(c, s, c->vel_host.data() + a * plane);
+        if (st) return st;
+        CUDA_TRY(c, cudaMemcpy(s.A + c->R * pf, hA.data() + a * pf, (size_t)(s.nz * pf) * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(c, cudaMemcpy(s.B + c->R * pf, hB.data() + a * pf, (size_t)(s.nz * pf) * 4, cudaMemcpyHostToDevice));
+    }
+    return FD_OK;
+}
+
+static fd_status prepare(fd_ctx *c) {
+    fd_status st = split_virtual(c, c->opt_vslabs);
+    if (st) return st;
+    c->vel_host.clear();
+    c->vel_host.shrink_to_fit();
+    int64_t maxnz = 0;
+    for (auto &s : c->slabs) maxnz = std::max(maxnz, s.nz);
+    if (c->opt_kernel != 1) {
+        choose_tile(c, maxnz);
+        if (c->tile < 0) return fail(FD_ERR_CUDA, "no fused kernel configuration fits this device");
+        const TileCfg &t = tile_table()[c->tile];
+        CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
+    }
+    const bool dist = c->nranks > 1;
+    for (auto &s : c->slabs) {
+        if (c->opt_kernel != 1) {
+            st = make_maps(c, s);
+            if (st) return st;
+        }
+        s.regions.clear();
+        const int32_t nz = (int32_t)s.nz, R = c->R;
+        auto add = [&](int32_t lo, int32_t hi, bool boundary) {
+            if (hi <= lo) return;
+            Region g;
+            g.zlo = lo; g.zhi = hi; g.boundary = boundary;
+            g.zchunks = (c->opt_kernel == 1) ? 1 : chunks_for(c, tile_table()[c->tile], c->occ, hi - lo);
+            s.regions.push_back(g);
+        };
+        if (dist && c->opt_kernel != 1) {
+            // boundary planes first (they feed the exchange), interior overlaps it
+            const int32_t lo_end = c->rank > 0 ? R : 0;
+            const int32_t hi_beg = c->rank < c->nranks - 1 ? nz - R : nz;
+            if (c->rank > 0) add(0, R, true);
+            if (c->rank < c->nranks - 1) add(nz - R, nz, true);
+            add(lo_end, hi_beg, false);
+        } else {
+            add(0, nz, false);
+        }
+        for (auto &g : s.regions) {
+            st = upload_region_receivers(c, s, g);
+            if (st) return st;
+        }
+    }
+    if (dist) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        CUDA_TRY(c, cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+        ncclResult_t r = nccl().CommInitRank(&c->comm, c->nranks, c->nccl_id, c->rank);
+        if (r != 0) {
+            c->poisoned = true;
+            return fail(FD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+        }
+    }
     return FD_OK;
 }
 
@@ -432,6 +633,7 @@ static fd_status ensure_traces(fd_ctx *c, int64_t steps_needed) {
     cap = std::max<int64_t>(cap, 16);
     float *nb = (float *)dev_alloc((size_t)(cap * nrec) * 4);
     if (!nb) return fail(FD_ERR_NOMEM, "trace buffer allocation failed");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     CUDA_TRY(c, cudaMemsetAsync(nb, 0, (size_t)(cap * nrec) * 4, c->stream));
     if (c->d_traces) {
         CUDA_TRY(c, cudaMemcpyAsync(nb, c->d_traces, (size_t)(c->trace_cap * nrec) * 4, cudaMemcpyDeviceToDevice,
@@ -444,95 +646,170 @@ static fd_status ensure_traces(fd_ctx *c, int64_t steps_needed) {
     return FD_OK;
 }
 
-static void fill_params(fd_ctx *c, StepParams &p, int64_t step_k) {
+// Kernel parameters of one launch (region g of slab s) for step k.
+static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepParams &p, int64_t step_k) {
     memset(&p, 0, sizeof p);
-    p.nx = c->nxg; p.ny = c->nyg; p.nz = c->nz;
-    p.pitch = c->pitch; p.gz0 = c->z0; p.nzg = c->nzg;
-    p.zlo = 0; p.zhi = (int32_t)c->nz;
+    p.nx = c->nxg; p.ny = c->nyg; p.nz = s.nz;
+    p.pitch = c->pitch; p.gz0 = s.z0; p.nzg = c->nzg;
+    p.zlo = g ? g->zlo : 0;
+    p.zhi = g ? g->zhi : (int32_t)s.nz;
+    p.nchunks = g ? g->zchunks : 1;
     p.nsrc = (int32_t)c->src.size();
-    for (int s = 0; s < p.nsrc; ++s) {
-        p.sz[s] = (int32_t)(c->src[s].g[0] - c->z0);
-        p.sy[s] = (int32_t)c->src[s].g[1];
-        p.sx[s] = (int32_t)c->src[s].g[2];
+    for (int q = 0; q < p.nsrc; ++q) {
+        p.sz[q] = (int32_t)(c->src[q].g[0] - s.z0);
+        p.sy[q] = (int32_t)c->src[q].g[1];
+        p.sx[q] = (int32_t)c->src[q].g[2];
         // w_{k+1}: the value injected into P^{k+1} by this launch (eager form)
-        p.w[s] = (float)(c->src[s].amp * ricker((double)(step_k + 1) * c->dt, c->src[s].f, c->src[s].t0));
+        p.w[q] = (float)(c->src[q].amp * ricker((double)(step_k + 1) * c->dt, c->src[q].f, c->src[q].t0));
     }
-    p.src_raw = c->d_src_raw;
-    const int n = c->nrec_local;
-    if (c->d_rec) {
-        p.rec.z = c->d_rec;
-        p.rec.y = c->d_rec + n;
-        p.rec.x = c->d_rec + 2 * n;
-        p.rec.id = c->d_rec + 3 * n;
-        p.rec.off = (c->opt_kernel == 1) ? nullptr : c->d_rec + 4 * n;
+    p.src_raw = s.d_src_raw;
+    if (g && g->d_rec) {
+        const int n = g->nrec;
+        p.rec.z = g->d_rec;
+        p.rec.y = g->d_rec + n;
+        p.rec.x = g->d_rec + 2 * n;
+        p.rec.id = g->d_rec + 3 * n;
+        p.rec.off = (c->opt_kernel == 1) ? nullptr : g->d_rec + 4 * n;
+        p.nrec_local = n;
     }
-    p.nrec_local = n;
-    p.trace_row = c->d_traces ? c->d_traces + step_k * (int64_t)c->rec.size() : nullptr;
+    p.trace_row = (c->d_traces && step_k >= 0) ? c->d_traces + step_k * (int64_t)c->rec.size() : nullptr;
 }
 
-template <int R> static void launch_inject(fd_ctx *c, float *field, const StepParams &p) {
-    inject_kernel<R><<<1, 32, 0, c->stream>>>(field, p);
+template <int R> static void launch_inject(cudaStream_t st, float *field, const StepParams &p) {
+    inject_kernel<R><<<1, 32, 0, st>>>(field, p);
 }
-template <int R, int NDIM> static void launch_naive(fd_ctx *c, const StepParams &p) {
-    const int64_t total = c->nxg * c->nyg * c->nz;
+template <int R, int NDIM> static void launch_naive(const fd_ctx *c, const Slab &s, cudaStream_t st,
+                                                    const StepParams &p) {
+    const int64_t total = c->nxg * c->nyg * s.nz;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    naive_step_kernel<R, NDIM><<<blocks, 256, 0, c->stream>>>(p);
+    naive_step_kernel<R, NDIM><<<blocks, 256, 0, st>>>(p);
 }
-template <int R> static void launch_gather(fd_ctx *c, const StepParams &p) {
-    gather_receivers_kernel<R><<<(c->nrec_local + 127) / 128, 128, 0, c->stream>>>(p);
+template <int R> static void launch_gather(cudaStream_t st, int n, const StepParams &p) {
+    gather_receivers_kernel<R><<<(n + 127) / 128, 128, 0, st>>>(p);
 }
 
-static void dispatch_inject(fd_ctx *c, float *field, const StepParams &p) {
+static void dispatch_inject(fd_ctx *c, cudaStream_t st, float *field, const StepParams &p) {
     switch (c->R) {
-    case 1: launch_inject<1>(c, field, p); break;
-    case 2: launch_inject<2>(c, field, p); break;
-    case 3: launch_inject<3>(c, field, p); break;
-    default: launch_inject<4>(c, field, p); break;
+    case 1: launch_inject<1>(st, field, p); break;
+    case 2: launch_inject<2>(st, field, p); break;
+    case 3: launch_inject<3>(st, field, p); break;
+    default: launch_inject<4>(st, field, p); break;
     }
     ++c->launches;
 }
 
-static fd_status one_step(fd_ctx *c) {
+static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     StepParams p;
-    fill_params(c, p, c->k);
-    float *cur = cur_buf(c), *prev = prev_buf(c);
+    fill_params(c, s, &g, p, c->k);
+    float *cur = cur_buf(c, s), *prev = prev_buf(c, s);
     p.pnext = prev;
     p.p = cur;
-    p.K = c->K;
+    p.K = s.K;
     if (c->opt_kernel == 1) {
         // naive path: stencil, receivers, injection (three launches)
         switch (c->R * 10 + c->ndim) {
-        case 12: launch_naive<1, 2>(c, p); break;
-        case 13: launch_naive<1, 3>(c, p); break;
-        case 22: launch_naive<2, 2>(c, p); break;
-        case 23: launch_naive<2, 3>(c, p); break;
-        case 32: launch_naive<3, 2>(c, p); break;
-        case 33: launch_naive<3, 3>(c, p); break;
-        case 42: launch_naive<4, 2>(c, p); break;
-        default: launch_naive<4, 3>(c, p); break;
+        case 12: launch_naive<1, 2>(c, s, st, p); break;
+        case 13: launch_naive<1, 3>(c, s, st, p); break;
+        case 22: launch_naive<2, 2>(c, s, st, p); break;
+        case 23: launch_naive<2, 3>(c, s, st, p); break;
+        case 32: launch_naive<3, 2>(c, s, st, p); break;
+        case 33: launch_naive<3, 3>(c, s, st, p); break;
+        case 42: launch_naive<4, 2>(c, s, st, p); break;
+        default: launch_naive<4, 3>(c, s, st, p); break;
         }
         ++c->launches;
-        if (c->nrec_local > 0) {
+        if (g.nrec > 0) {
             switch (c->R) {
-            case 1: launch_gather<1>(c, p); break;
-            case 2: launch_gather<2>(c, p); break;
-            case 3: launch_gather<3>(c, p); break;
-            default: launch_gather<4>(c, p); break;
+            case 1: launch_gather<1>(st, g.nrec, p); break;
+            case 2: launch_gather<2>(st, g.nrec, p); break;
+            case 3: launch_gather<3>(st, g.nrec, p); break;
+            default: launch_gather<4>(st, g.nrec, p); break;
             }
             ++c->launches;
         }
-        if (p.nsrc > 0) dispatch_inject(c, prev, p);
+        if (p.nsrc > 0) dispatch_inject(c, st, prev, p);
+        return;
+    }
+    const TileCfg &t = tile_table()[c->tile];
+    p.ntx = (int32_t)((c->nxg + t.tx - 1) / t.tx);
+    p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
+    const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
+    g.ctas = (int)grid.x;
+    const CUtensorMap &mp = c->cur_is_A ? s.mA_halo : s.mB_halo;
+    const CUtensorMap &mpp = c->cur_is_A ? s.mB_tile : s.mA_tile;
+    t.launch(grid, t.smem, st, mp, mpp, s.mK, p);
+    ++c->launches;
+}
+
+// Halo exchange of the field that becomes P (buffer `which_next`: true = the
+// p_next buffer of the step just launched, false = the current buffer).
+// Virtual slabs: device copies on the user stream.  Ranks: NCCL send/recv of
+// r planes per face on the comm stream (owned planes [0,r) and [nz-r,nz) live
+// at buffer planes [r,2r) and [nz,nz+r); halos at [0,r) and [nz+r,nz+2r)).
+static fd_status exchange(fd_ctx *c, bool next, cudaStream_t st) {
+    const int64_t pf = plane_floats(c), R = c->R;
+    const size_t cnt = (size_t)(R * pf);
+    if (c->nranks > 1) {
+        Slab &s = c->slabs[0];
+        float *buf = next ? prev_buf(c, s) : cur_buf(c, s);
+        NcclApi &n = nccl();
+        ncclResult_t r = n.GroupStart();
+        if (c->rank > 0) {
+            if (!r) r = n.Send(buf + R * pf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
+            if (!r) r = n.Recv(buf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
+        }
+        if (c->rank < c->nranks - 1) {
+            if (!r) r = n.Send(buf + s.nz * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
+            if (!r) r = n.Recv(buf + (s.nz + R) * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
+        }
+        ncclResult_t r2 = n.GroupEnd();
+        if (r || r2) {
+            c->poisoned = true;
+            return fail(FD_ERR_NCCL, "NCCL halo exchange: %s", n.GetErrorString(r ? r : r2));
+        }
+        return FD_OK;
+    }
+    for (size_t q = 0; q < c->slabs.size(); ++q) {
+        Slab &s = c->slabs[q];
+        float *buf = next ? prev_buf(c, s) : cur_buf(c, s);
+        if (q > 0) {
+            Slab &l = c->slabs[q - 1];
+            const float *lb = next ? prev_buf(c, l) : cur_buf(c, l);
+            CUDA_TRY(c, cudaMemcpyAsync(buf, lb + l.nz * pf, cnt * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        if (q + 1 < c->slabs.size()) {
+            Slab &u = c->slabs[q + 1];
+            const float *ub = next ? prev_buf(c, u) : cur_buf(c, u);
+            CUDA_TRY(c, cudaMemcpyAsync(buf + (s.nz + R) * pf, ub + R * pf, cnt * 4, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return FD_OK;
+}
+
+static fd_status one_step(fd_ctx *c) {
+    fd_status s;
+    if (c->nranks > 1 && c->opt_kernel != 1) {
+        // comm stream: boundary planes -> NCCL exchange; user stream: interior.
+        // Step k+1 starts after both (its boundary kernel overwrites planes
+        // that step k's interior kernel reads as p).
+        Slab &sl = c->slabs[0];
+        CUDA_TRY(c, cudaEventRecord(c->ev_step, c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
+        for (auto &g : sl.regions)
+            if (g.boundary) launch_region(c, sl, g, c->comm_stream);
+        s = exchange(c, true, c->comm_stream);
+        if (s) return s;
+        CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
+        for (auto &g : sl.regions)
+            if (!g.boundary) launch_region(c, sl, g, c->stream);
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     } else {
-        const TileCfg &t = tile_table()[c->tile];
-        p.ntx = (int32_t)((c->nxg + t.tx - 1) / t.tx);
-        p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
-        p.nchunks = c->zchunks;
-        const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
-        c->ctas = (int)grid.x;
-        const CUtensorMap &mp = c->cur_is_A ? c->mapA_halo : c->mapB_halo;
-        const CUtensorMap &mpp = c->cur_is_A ? c->mapB_tile : c->mapA_tile;
-        t.launch(grid, t.smem, c->stream, mp, mpp, c->mapK, p);
-        ++c->launches;
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.regions) launch_region(c, sl, g, c->stream);
+        if (c->slabs.size() > 1 || c->nranks > 1) {
+            s = exchange(c, true, c->stream);
+            if (s) return s;
+        }
     }
     CUDA_TRY(c, cudaGetLastError());
     c->cur_is_A = !c->cur_is_A;
@@ -545,16 +822,14 @@ extern "C" {
 
 fd_status fd_create(fd_ctx **out, int ndim, const int64_t *dims, double h, double dt, int order, const float *vel,
                     uint32_t flags) {
-    return create_impl(out, ndim, dims, h, dt, order, vel, flags, 0, 1, -1, 0);
+    return create_impl(out, ndim, dims, h, dt, order, vel, flags, 0, 1, -1, 0, nullptr);
 }
 
 fd_status fd_create_dist(fd_ctx **out, int ndim, const int64_t *global_dims, double h, double dt, int order,
                          const float *vel, uint32_t flags, const fd_dist *dist) {
     if (!dist) return fail(FD_ERR_ARG, "dist is NULL");
-    if (dist->nranks > 1)
-        return fail(FD_ERR_NCCL, "multi-rank NCCL contexts are not available in this build");
     return create_impl(out, ndim, global_dims, h, dt, order, vel, flags, dist->rank, dist->nranks, dist->device,
-                       dist->vel_is_slab);
+                       dist->vel_is_slab, dist->nccl_id);
 }
 
 fd_status fd_partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *z1) {
@@ -563,7 +838,13 @@ fd_status fd_partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *z
 
 fd_status fd_nccl_get_unique_id(void *out128) {
     if (!out128) return fail(FD_ERR_ARG, "out128 is NULL");
-    return fail(FD_ERR_NCCL, "NCCL support is not available in this build");
+    NcclApi &n = nccl();
+    if (!n.ok) return fail(FD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+    ncclUniqueId id;
+    ncclResult_t r = n.GetUniqueId(&id);
+    if (r) return fail(FD_ERR_NCCL, "ncclGetUniqueId: %s", n.GetErrorString(r));
+    memcpy(out128, &id, sizeof id);
+    return FD_OK;
 }
 
 static fd_status check_ctx(fd_ctx *c) {
@@ -620,17 +901,22 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
     if (!c->started) {
         s = prepare(c);
         if (s) return s;
-        s = upload_receivers(c);
-        if (s) return s;
         c->started = true;
     }
     s = ensure_traces(c, c->k + n);
     if (s) return s;
     if (!c->injected) {
-        // add_source of step k on the current field; later injections are eager
-        StepParams p;
-        fill_params(c, p, c->k - 1);   // w_{(k-1)+1} = w_k
-        if (p.nsrc > 0) dispatch_inject(c, cur_buf(c), p);
+        // add_source of step k on the current field by the owning slab;
+        // later injections are eager.  Then refresh the halos of P.
+        for (auto &sl : c->slabs) {
+            StepParams p;
+            fill_params(c, sl, nullptr, p, c->k - 1);   // w_{(k-1)+1} = w_k
+            if (p.nsrc > 0) dispatch_inject(c, c->stream, cur_buf(c, sl), p);
+        }
+        if (c->slabs.size() > 1 || c->nranks > 1) {
+            s = exchange(c, false, c->stream);
+            if (s) return s;
+        }
         c->injected = true;
     }
     for (int64_t i = 0; i < n; ++i) {
@@ -638,6 +924,14 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         if (s) return s;
     }
     if (!c->opt_async) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->comm && nccl().CommGetAsyncError) {
+        ncclResult_t ae = 0;
+        nccl().CommGetAsyncError(c->comm, &ae);
+        if (ae) {
+            c->poisoned = true;
+            return fail(FD_ERR_NCCL, "NCCL async error: %s", nccl().GetErrorString(ae));
+        }
+    }
     return FD_OK;
 }
 
@@ -646,20 +940,23 @@ fd_status fd_get_wavefield(fd_ctx *c, int which, float *host_out) {
     if (s) return s;
     if (!host_out) return fail(FD_ERR_ARG, "host_out is NULL");
     if (which != FD_FIELD_CUR && which != FD_FIELD_PREV) return fail(FD_ERR_ARG, "which must be CUR or PREV");
-    const float *buf = which == FD_FIELD_CUR ? cur_buf(c) : prev_buf(c);
-    const float *src = buf + (int64_t)c->R * c->nyg * c->pitch;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    CUDA_TRY(c, cudaMemcpy2D(host_out, c->nxg * 4, src, c->pitch * 4, c->nxg * 4, c->nyg * c->nz,
-                             cudaMemcpyDeviceToHost));
-    if (which == FD_FIELD_CUR && c->injected && !c->src.empty()) {
-        // the CUR buffer already holds w_k (eager injection): restore the raw
-        // P^k at each source point from the value recorded before its first add
-        std::vector<float> raw(c->src.size());
-        CUDA_TRY(c, cudaMemcpy(raw.data(), c->d_src_raw, raw.size() * 4, cudaMemcpyDeviceToHost));
-        for (int s2 = (int)c->src.size() - 1; s2 >= 0; --s2) {
-            const int64_t gz = c->src[s2].g[0];
-            if (gz < c->z0 || gz >= c->z1) continue;
-            host_out[((gz - c->z0) * c->nyg + c->src[s2].g[1]) * c->nxg + c->src[s2].g[2]] = raw[s2];
+    const int64_t pf = plane_floats(c);
+    for (auto &sl : c->slabs) {
+        const float *buf = which == FD_FIELD_CUR ? cur_buf(c, sl) : prev_buf(c, sl);
+        float *dst = host_out + (sl.z0 - c->z0) * c->nyg * c->nxg;
+        CUDA_TRY(c, cudaMemcpy2D(dst, c->nxg * 4, buf + (int64_t)c->R * pf, c->pitch * 4, c->nxg * 4,
+                                 c->nyg * sl.nz, cudaMemcpyDeviceToHost));
+        if (which == FD_FIELD_CUR && c->injected && !c->src.empty()) {
+            // the CUR buffer already holds w_k (eager injection): restore the raw
+            // P^k at each source point from the value recorded before its first add
+            std::vector<float> raw(c->src.size());
+            CUDA_TRY(c, cudaMemcpy(raw.data(), sl.d_src_raw, raw.size() * 4, cudaMemcpyDeviceToHost));
+            for (int q = (int)c->src.size() - 1; q >= 0; --q) {
+                const int64_t gz = c->src[q].g[0];
+                if (gz < sl.z0 || gz >= sl.z1) continue;
+                host_out[((gz - c->z0) * c->nyg + c->src[q].g[1]) * c->nxg + c->src[q].g[2]] = raw[q];
+            }
         }
     }
     return FD_OK;
@@ -671,8 +968,8 @@ fd_status fd_get_traces(fd_ctx *c, float *host_out, int64_t cap, int64_t *nsteps
     if (!host_out || !nsteps_out) return fail(FD_ERR_ARG, "host_out/nsteps_out is NULL");
     const int64_t nrec = (int64_t)c->rec.size();
     if (nrec == 0) return fail(FD_ERR_STATE, "no receivers registered");
-    if (cap < nrec * c->k) return fail(FD_ERR_STATE, "cap %lld < nrec*nsteps = %lld", (long long)cap,
-                                       (long long)(nrec * c->k));
+    if (cap < nrec * c->k)
+        return fail(FD_ERR_STATE, "cap %lld < nrec*nsteps = %lld", (long long)cap, (long long)(nrec * c->k));
     *nsteps_out = c->k;
     if (c->k == 0) return FD_OK;
     std::vector<float> tmp((size_t)(nrec * c->k));
@@ -689,7 +986,8 @@ fd_status fd_get_traces(fd_ctx *c, float *host_out, int64_t cap, int64_t *nsteps
 fd_status fd_destroy(fd_ctx *c) {
     if (!c) return FD_OK;
     if (c->stream) cudaStreamSynchronize(c->stream);
-    destroy_buffers(c);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    destroy_all(c);
     delete c;
     std::lock_guard<std::mutex> lk(g_mu);
     --g_live_contexts;
@@ -735,9 +1033,13 @@ fd_status fd_set_wavefield(fd_ctx *c, int which, const float *host_in) {
     if (!host_in) return fail(FD_ERR_ARG, "host_in is NULL");
     if (which != FD_FIELD_CUR && which != FD_FIELD_PREV) return fail(FD_ERR_ARG, "which must be CUR or PREV");
     if (c->started) return fail(FD_ERR_STATE, "fd_set_wavefield only before the first fd_step");
-    float *buf = which == FD_FIELD_CUR ? cur_buf(c) : prev_buf(c);
-    CUDA_TRY(c, cudaMemcpy2D(buf + (int64_t)c->R * c->nyg * c->pitch, c->pitch * 4, host_in, c->nxg * 4,
-                             c->nxg * 4, c->nyg * c->nz, cudaMemcpyHostToDevice));
+    const int64_t pf = plane_floats(c);
+    for (auto &sl : c->slabs) {
+        float *buf = which == FD_FIELD_CUR ? cur_buf(c, sl) : prev_buf(c, sl);
+        CUDA_TRY(c, cudaMemcpy2D(buf + (int64_t)c->R * pf, c->pitch * 4,
+                                 host_in + (sl.z0 - c->z0) * c->nyg * c->nxg, c->nxg * 4, c->nxg * 4,
+                                 c->nyg * sl.nz, cudaMemcpyHostToDevice));
+    }
     return FD_OK;
 }
 
@@ -748,7 +1050,7 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
     switch (key) {
     case FD_OPT_KERNEL:
         if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_KERNEL must be 0, 1 or 2");
-        c->opt_kernel = (int)v == 2 ? 0 : (int)v;
+        c->opt_kernel = (v == 2) ? 0 : (int)v;
         return FD_OK;
     case FD_OPT_TILE: {
         const auto &tab = tile_table();
@@ -765,8 +1067,9 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
     case FD_OPT_ASYNC: c->opt_async = v ? 1 : 0; return FD_OK;
     case FD_OPT_GRAPH: c->opt_graph = v ? 1 : 0; return FD_OK;
     case FD_OPT_VSLABS:
-        if (v != 1) return fail(FD_ERR_ARG, "virtual slabs are not available in this build");
-        c->opt_vslabs = 1;
+        if (v < 1 || v > 64) return fail(FD_ERR_ARG, "FD_OPT_VSLABS must be in [1, 64]");
+        if (c->nranks > 1 && v != 1) return fail(FD_ERR_ARG, "FD_OPT_VSLABS is for single-process contexts");
+        c->opt_vslabs = (int)v;
         return FD_OK;
     default: return fail(FD_ERR_ARG, "unknown option %d", key);
     }
@@ -779,7 +1082,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     memset(o, 0, sizeof *o);
     o->steps_done = c->k;
     o->kernel_launches = c->launches;
-    o->local_dims[0] = c->nz;
+    o->local_dims[0] = c->z1 - c->z0;
     if (c->ndim == 3) { o->local_dims[1] = c->nyg; o->local_dims[2] = c->nxg; }
     else o->local_dims[1] = c->nxg;
     o->z0 = c->z0; o->z1 = c->z1;
@@ -787,15 +1090,19 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->order = c->order;
     o->device_bytes = c->dev_bytes;
     if (c->opt_kernel == 1) { o->kernel = 1; return FD_OK; }
-    if (!c->maps_ready) choose_config(c, c->nz);
     o->kernel = 2;
+    if (!c->started) choose_tile(c, c->z1 - c->z0);
     if (c->tile >= 0) {
         const TileCfg &t = tile_table()[c->tile];
         o->tile_x = t.tx; o->tile_y = t.ty; o->rows_per_thread = t.ny;
         o->p_stages = t.r + 1 + t.dp; o->k_stages = t.dk + 1;
         o->threads_per_cta = t.threads; o->smem_bytes = t.smem;
-        o->zchunks = c->zchunks;
-        o->ctas = (int)(((c->nxg + t.tx - 1) / t.tx) * ((c->nyg + t.ty - 1) / t.ty) * c->zchunks);
+        int ctas = 0, zc = 0;
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.regions) { ctas += (int)(ntiles_of(c, t) * g.zchunks); zc = std::max(zc, g.zchunks); }
+        if (!c->started) { zc = chunks_for(c, t, c->occ, c->z1 - c->z0); ctas = (int)(ntiles_of(c, t) * zc); }
+        o->ctas = ctas;
+        o->zchunks = zc;
     }
     return FD_OK;
 }
