@@ -185,29 +185,49 @@ def run_reference(args, wl):
 
 
 # ------------------------------------------------------------------ GPU side
+def _make_sim(wl, world, stream=None, options=None):
+    """This rank's simulation of the workload: the whole grid at N=1; at N>1 a
+    z-slab of the weak-scaled grid (N copies of the workload's grid stacked
+    along z, slab-decomposed, halo exchange over NCCL inside libfd.so)."""
+    import paper_2311_05038_b200 as fd
+    from workloads import velocity
+    if world == 1:
+        vel = wl.vel()
+        sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream, options=options)
+        nbytes = vel.nbytes
+    else:
+        from paper_2311_05038_b200 import dist as fdd
+        import torch.distributed as dist
+        gdims = (wl.dims[0] * world,) + tuple(wl.dims[1:])
+        z0, z1 = fdd.partition(gdims[0], world, dist.get_rank())
+        vel = velocity(wl.model, gdims, z0, z1)
+        sim = fdd.create(vel, gdims, wl.h, wl.dt, wl.order, device=int(os.environ.get("LOCAL_RANK", "0")),
+                         stream=stream, options=options)
+        nbytes = vel.nbytes
+    for s in wl.sources:
+        sim.add_source(s.idx, s.f, s.t0, s.amp)
+    sim.set_receivers(wl.receivers)
+    return sim, nbytes
+
+
 def run_ours(args, wl):
     import torch
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2311_05038_b200 as fd
-    from paper_2311_05038_b200 import fd as fdm
 
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    # weak scaling: every rank runs the configured grid (N independent replicas
-    # until the slab-decomposed path lands)
-    vel = wl.vel()
     stream = torch.cuda.Stream(device=dev)
-    sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream.cuda_stream,
-                        options={fd.FD_OPT_ASYNC: 1})
-    for s in wl.sources:
-        sim.add_source(s.idx, s.f, s.t0, s.amp)
-    sim.set_receivers(wl.receivers)
+    sim, _ = _make_sim(wl, world, stream=stream.cuda_stream, options={fd.FD_OPT_ASYNC: 1})
     sim.step(args.warmup)
     stream.synchronize()
     launches0 = sim.info()["kernel_launches"]
+    # per-launch CUDA events on the library's stream for the roofline's kernel time
+    fd.fd_set_option(sim.ctx, fd.FD_OPT_PROFILE, 1)
+    sim.reset_kernel_times()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -219,9 +239,12 @@ def run_ours(args, wl):
         ev1.record(stream)
         ev1.synchronize()
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
     info = sim.info()
     launches = info["kernel_launches"] - launches0
+    ktimes = sim.kernel_times()
     T = sim.traces()
     finite = bool(np.all(np.isfinite(T)))
     sim.close()
@@ -234,34 +257,42 @@ def run_ours(args, wl):
 
     # e2e through the public API with host buffers: create (H2D of the model),
     # K steps, traces + final wavefield read back (D2H)
-    e2e = None
     if args.no_e2e:
-        return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, None)
+        return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, None, ktimes)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    with fd.Simulation(vel, wl.h, wl.dt, wl.order) as s2:
-        for s in wl.sources:
-            s2.add_source(s.idx, s.f, s.t0, s.amp)
-        s2.set_receivers(wl.receivers)
-        s2.step(args.steps)
-        T2 = s2.traces()
-        W2 = s2.wavefield()
+    s2, h2d = _make_sim(wl, world)
+    s2.step(args.steps)
+    T2 = s2.traces()
+    W2 = s2.wavefield()
+    s2.close()
     e2e_s = time.perf_counter() - t0
-    h2d = vel.nbytes + 8 * len(wl.receivers) * wl.ndim
+    if world > 1:
+        from paper_2311_05038_b200 import dist as fdd
+        e2e_s = fdd.max_over_ranks(e2e_s)
+    h2d += 8 * len(wl.receivers) * wl.ndim
     d2h = T2.nbytes + W2.nbytes
     e2e = {"value": wl.npts * args.steps * world / e2e_s / 1e9, "unit": "Gpts/s",
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": e2e_s}
-    return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e)
+    return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes)
 
 
-def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e):
+def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes):
     peak, peak_src = _peaks()
-    achieved = BYTES_PER_POINT * wl.npts / (ms_step / 1e3) / 1e9
+    # dominant kernel: the fused step kernel, one launch per step; its average
+    # launch duration from the events around each launch in the timed region
+    kms, kn = ktimes.get("fused", (ms_step * args.steps, args.steps))
+    k_avg_s = kms / kn / 1e3
+    achieved = BYTES_PER_POINT * wl.npts / k_avg_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": _ncu_traffic(wl.name, wl.order), "peak_source": peak_src,
             "algorithmic_bytes_per_point": BYTES_PER_POINT, "points_per_launch": wl.npts,
-            "kernel": "fused_step_kernel"}
+            "kernel": "fused_step_kernel" if wl.ndim == 3 else "tile2d_step_kernel",
+            "kernel_ms_per_launch": k_avg_s * 1e3, "kernel_share_of_step": min(1.0, k_avg_s * 1e3 / ms_step),
+            "kernel_times_ms": {k: v[0] for k, v in ktimes.items()}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, desc = cpu_oracle_sample(wl, args.cpu_budget)
@@ -273,7 +304,8 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
         "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
                    "dt": wl.dt, "h": wl.h, "receivers": len(wl.receivers), "sources": len(wl.sources),
                    "l2": "no flush: per-step working set %.2f GB >> 126 MB L2" % (12.0 * wl.npts / 1e9),
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "parallelism": f"z-slabs x{world} (NCCL halo exchange)" if world > 1 else "1 GPU",
+                   "global_grid": [wl.dims[0] * world] + list(wl.dims[1:]),
                    "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "traces_finite": finite,

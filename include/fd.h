@@ -158,17 +158,30 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
 
 /* Tuning / debug options; set before the first fd_step (else FD_ERR_STATE).
  *   FD_OPT_KERNEL    0 auto (fused TMA kernel), 1 naive reference kernels (debug,
- *                    three launches per step), 2 fused TMA kernel
+ *                    three launches per step), 2 fused TMA kernel, 3 the paper's
+ *                    unfused decomposition (Listing 3: fd_pzz, [fd_pyy], fd_pxx,
+ *                    fd_time as separate kernels with derivative fields; the
+ *                    Fig. 5 experiment); all bitwise equal
  *   FD_OPT_TILE      index into the compiled tile table (-1 = auto); see fd_get_info
  *   FD_OPT_ZCHUNKS   z-chunks per x-y tile column (0 = auto)
  *   FD_OPT_ASYNC     1: fd_step returns without synchronising the stream
  *   FD_OPT_GRAPH     1: replay fd_step's launches from CUDA graphs (default 1)
  *   FD_OPT_VSLABS    n >= 1: split the grid into n z-slabs on this one GPU with
  *                    device-copy halo exchange (tests the slab logic)
- * Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
+ *   FD_OPT_PROFILE   1: bracket every launch with CUDA events (fd_get_kernel_times)
+ * FD_OPT_ASYNC and FD_OPT_PROFILE may change at any time; the others only before
+ * the first fd_step.  Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
 enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
-       FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6 };
+       FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7 };
 fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
+
+/* Device time per kernel kind accumulated while FD_OPT_PROFILE = 1 (ms and launch
+ * counts, arrays of FD_K_COUNT).  Synchronises with the pending events.
+ * FD_K_HALO times the halo exchange (copies / NCCL), not a kernel of ours. */
+enum { FD_K_FUSED = 0, FD_K_NAIVE = 1, FD_K_GATHER = 2, FD_K_INJECT = 3, FD_K_PXX = 4,
+       FD_K_PYY = 5, FD_K_PZZ = 6, FD_K_TIME = 7, FD_K_HALO = 8, FD_K_COUNT = 9 };
+fd_status fd_get_kernel_times(fd_ctx *ctx, double *ms, int64_t *launches);
+fd_status fd_reset_kernel_times(fd_ctx *ctx);
 
 /* Introspection (bench / tests). */
 typedef struct {
@@ -177,7 +190,7 @@ typedef struct {
     int64_t local_dims[3];     /* slow->fast (unused trailing entries 0)                 */
     int64_t z0, z1;            /* owned global planes                                    */
     int64_t pitch;             /* floats per stored row (>= nx, multiple of 32)          */
-    int kernel;                /* 1 naive, 2 fused TMA                                   */
+    int kernel;                /* 1 naive, 2 fused TMA, 3 unfused decomposition          */
     int tile_x, tile_y, rows_per_thread, p_stages, k_stages;
     int ctas, threads_per_cta, smem_bytes, zchunks;
     int order;

@@ -65,16 +65,29 @@ struct StepParams {
     float *pnext;           // base of the p_prev buffer (overwritten in place)
     const float *p;         // base of the p buffer (naive kernel only)
     const float *K;         // K base (naive kernel only)
+    // step index: k, or *kdev + koff when replayed from a CUDA graph
+    int64_t k;
+    const int64_t *kdev;
+    int32_t koff;
     // eager source injection of w_{k+1}
     int32_t nsrc;
     int32_t sz[kMaxSources], sy[kMaxSources], sx[kMaxSources];   // local coords (sz may be outside)
-    float w[kMaxSources];
+    const float *wtab;      // w_j of source s at wtab[j * nsrc + s] (fp64 Ricker, rounded once)
     float *src_raw;         // [nsrc] raw p_next before the s-th injection
     // receivers
     Receivers rec;
     int32_t nrec_local;     // receivers of this launch's list (naive gather)
-    float *trace_row;       // traces + k * nrec_total
+    float *traces;          // step-major [k][nrec_total]
+    int32_t nrec_total;
 };
+
+__device__ __forceinline__ int64_t step_index(const StepParams &p) { return p.kdev ? *p.kdev + p.koff : p.k; }
+__device__ __forceinline__ float *trace_row_of(const StepParams &p, int64_t k) {
+    return p.traces ? p.traces + k * p.nrec_total : nullptr;
+}
+__device__ __forceinline__ const float *w_next_of(const StepParams &p, int64_t k) {
+    return p.wtab + (k + 1) * p.nsrc;   // w_{k+1}
+}
 
 // ------------------------------------------------------------------ PTX glue
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -260,6 +273,10 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     const int rend = prm.rec.off ? prm.rec.off[unit + 1] : 0;
     int rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
 
+    const int64_t kk = step_index(prm);
+    float *const trace_row = trace_row_of(prm, kk);
+    const float *const wn = w_next_of(prm, kk);
+
     float4 q[2 * R + 1][C::NY];
 #pragma unroll
     for (int i = 0; i < 2 * R + 1; ++i)
@@ -347,7 +364,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             if (dy >= 0 && dy < C::NY && dx >= 0 && dx < 4) {
 #pragma unroll
                 for (int yy = 0; yy < C::NY; ++yy)
-                    if (yy == dy) prm.trace_row[prm.rec.id[rp]] = f4(out[yy], dx);
+                    if (yy == dy) trace_row[prm.rec.id[rp]] = f4(out[yy], dx);
             }
             ++rp;
             rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
@@ -363,7 +380,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                         if (yy == dy) {
                             const float v = f4(out[yy], dx);
                             prm.src_raw[s2] = v;
-                            f4set(out[yy], dx, __fadd_rn(v, prm.w[s2]));
+                            f4set(out[yy], dx, __fadd_rn(v, wn[s2]));
                         }
                 }
             }
@@ -374,6 +391,165 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
                 if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 2D tile kernel
+// 2D grids (nz, nx): each CTA owns a column of TX x-points and a z-chunk of
+// row blocks; it streams TY-row blocks down z.  Each block is ONE TMA box of
+// (TX+8) x (TY+2r) p values (z halo rows included, re-read from L2) plus the
+// p_prev and K blocks, through an NS-slot mbarrier ring.  x taps and z taps
+// both come from SMEM (no register queue), in the canonical order: x term,
+// then z term (the 2D z axis plays the role of the 3D y axis of the tile).
+template <int R_, int TX_, int TY_, int NY_, int NS_>
+struct Cfg2 {
+    static constexpr int R = R_, TX = TX_, TY = TY_, NY = NY_, NS = NS_;
+    static constexpr int NDIM = 2;
+    static constexpr int BX = TX + 8, BZ = TY + 2 * R;
+    static constexpr int P_FLOATS = (BX * BZ + 31) / 32 * 32;
+    static constexpr int T_FLOATS = TX * TY;
+    static constexpr int STAGE = P_FLOATS + 2 * T_FLOATS;
+    static constexpr uint32_t STAGE_BYTES = (BX * BZ + 2 * T_FLOATS) * 4;
+    static constexpr int NTX = TX / 4, NTY = TY / NY;
+    static constexpr int NCONS = NTX * NTY, NWC = NCONS / 32, NTHREADS = NCONS + 32;
+    static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8 + 16;
+    // box shapes for the host (x, y, z): p (BX, 1, BZ), tiles (TX, 1, TY)
+    static constexpr int PBW = BX, TBW = TX, PBZ = BZ, TBZ = TY;
+    static_assert(BX <= 256 && BZ <= 256 && TY <= 256, "TMA box limit");
+    static_assert(TX % 4 == 0 && TY % NY == 0 && NCONS % 32 == 0, "tile");
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS)
+tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, 1, BZ)
+                   const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, 1, TY)
+                   const __grid_constant__ CUtensorMap map_k,    // K, box (TX, 1, TY)
+                   const StepParams prm) {
+    constexpr int R = C::R;
+    extern __shared__ __align__(128) float smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::NS * C::STAGE);
+    uint64_t *empty = full + C::NS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int unit = blockIdx.x;
+    const int chunk = unit / prm.ntx;
+    const int x0 = (unit - chunk * prm.ntx) * C::TX;
+    const int span = prm.zhi - prm.zlo;
+    const int nb = (span + C::TY - 1) / C::TY;
+    const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
+    const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
+    if (tid == 0) {
+        for (int i = 0; i < C::NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], C::NWC); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (b1 <= b0) return;
+    const int nload = b1 - b0;
+
+    if (warp == C::NWC) {
+        if (lane == 0) {
+            tma_prefetch_desc(&map_p); tma_prefetch_desc(&map_pp); tma_prefetch_desc(&map_k);
+            for (int l = 0; l < nload; ++l) {
+                const int s = l % C::NS;
+                const int rb = prm.zlo + (b0 + l) * C::TY;          // first local row of the block
+                mbar_wait(&empty[s], ((l / C::NS) & 1) ^ 1);
+                mbar_expect_tx(&full[s], C::STAGE_BYTES);
+                float *st = smem + s * C::STAGE;
+                tma_load_3d(st, &map_p, &full[s], x0 - 4, 0, rb);   // buffer plane (rb - R) + R
+                tma_load_3d(st + C::P_FLOATS, &map_pp, &full[s], x0, 0, rb + R);
+                tma_load_3d(st + C::P_FLOATS + C::T_FLOATS, &map_k, &full[s], x0, 0, rb);
+            }
+        }
+        return;
+    }
+
+    const int tx = tid % C::NTX, ty = tid / C::NTX;
+    const int xb = x0 + 4 * tx;
+    const int64_t nx = prm.nx;
+    bool inx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    uint32_t smask = 0;
+    const int zc0 = prm.zlo + b0 * C::TY, zc1 = min(prm.zhi, prm.zlo + b1 * C::TY);
+    for (int q = 0; q < prm.nsrc; ++q)
+        if (prm.sx[q] >= x0 && prm.sx[q] < x0 + C::TX && prm.sz[q] >= zc0 && prm.sz[q] < zc1) smask |= 1u << q;
+    int rp = prm.rec.off ? prm.rec.off[unit] : 0;
+    const int rend = prm.rec.off ? prm.rec.off[unit + 1] : 0;
+    int rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
+    constexpr float c0 = tap(R, 0);
+    const int64_t kk = step_index(prm);
+    float *const trace_row = trace_row_of(prm, kk);
+    const float *const wn = w_next_of(prm, kk);
+
+    for (int l = 0; l < nload; ++l) {
+        const int s = l % C::NS;
+        const int rb = prm.zlo + (b0 + l) * C::TY;
+        const int zt = rb + ty * C::NY;                   // first row of this thread
+        mbar_wait(&full[s], (l / C::NS) & 1);
+        const float *tp = smem + s * C::STAGE;
+        const float *tk = tp + C::P_FLOATS;
+        float4 col[C::NY + 2 * R];
+#pragma unroll
+        for (int i = 0; i < C::NY + 2 * R; ++i) col[i] = lds128(tp + (ty * C::NY + i) * C::BX + 4 + 4 * tx);
+        float4 out[C::NY];
+#pragma unroll
+        for (int yy = 0; yy < C::NY; ++yy) {
+            const float *row = tp + (ty * C::NY + yy + R) * C::BX + 4 * tx;
+            const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
+            const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+            const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
+            const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
+            const int64_t gz = prm.gz0 + zt + yy;
+            const bool inz = (gz >= R) && (gz < prm.nzg - R);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float pc = a[4 + e];
+                float sx = __fmul_rn(c0, pc);
+#pragma unroll
+                for (int m = 1; m <= R; ++m) sx = __fmaf_rn(tap(R, m), __fadd_rn(a[4 + e - m], a[4 + e + m]), sx);
+                float S = inx[e] ? sx : 0.f;
+                float sz = __fmul_rn(c0, pc);
+#pragma unroll
+                for (int m = 1; m <= R; ++m)
+                    sz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), sz);
+                S = inz ? __fadd_rn(S, sz) : S;
+                f4set(out[yy], e, __fmaf_rn(f4(kk4, e), S, __fmaf_rn(2.f, pc, -f4(pp4, e))));
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+
+        // receivers in this block (sorted by row), raw values before injection
+        while (rnext_z < rb + C::TY) {
+            const int dz = rnext_z - zt, dx = prm.rec.x[rp] - xb;
+            if (dz >= 0 && dz < C::NY && dx >= 0 && dx < 4) {
+#pragma unroll
+                for (int yy = 0; yy < C::NY; ++yy)
+                    if (yy == dz) trace_row[prm.rec.id[rp]] = f4(out[yy], dx);
+            }
+            ++rp;
+            rnext_z = (rp < rend) ? prm.rec.z[rp] : INT32_MAX;
+        }
+        if (smask) {
+            for (int q = 0; q < prm.nsrc; ++q) {
+                if (!((smask >> q) & 1u)) continue;
+                const int dz = prm.sz[q] - zt, dx = prm.sx[q] - xb;
+                if (dz >= 0 && dz < C::NY && dx >= 0 && dx < 4) {
+#pragma unroll
+                    for (int yy = 0; yy < C::NY; ++yy)
+                        if (yy == dz) {
+                            const float v = f4(out[yy], dx);
+                            prm.src_raw[q] = v;
+                            f4set(out[yy], dx, __fadd_rn(v, wn[q]));
+                        }
+                }
+            }
+        }
+        if (xb < prm.pitch) {
+            float *dst = prm.pnext + (int64_t)(zt + R) * prm.pitch + xb;
+#pragma unroll
+            for (int yy = 0; yy < C::NY; ++yy)
+                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
         }
     }
 }
@@ -424,26 +600,78 @@ __global__ void naive_step_kernel(const StepParams prm) {
     }
 }
 
+// ------------------------------------------------------------ unfused (paper's) decomposition
+// Listing 3's routines as separate kernels (the Fig. 5
+// experiment): fd_pzz / [fd_pyy] / fd_pxx each write one derivative field
+// (band = 0), fd_time combines them.  The derivative fields hold the
+// integer-tap sums (the 1/(scale h^2) lives in K), so
+//   S = (Pxx + Pyy) + Pzz  and  p_next = fma(K, S, fma(2, p, -p_prev))
+// equals the fused kernel's canonical expression (a band term contributes an
+// exact +0).  Fields are pitched like K (no halo planes).
+template <int R, int AXIS>   // AXIS 0 = x, 1 = y, 2 = z
+__global__ void d2_axis_kernel(const StepParams prm, float *__restrict__ out) {
+    const int64_t nx = prm.nx, ny = prm.ny, P = prm.pitch;
+    const int64_t npl = nx * ny, total = npl * prm.nz;
+    constexpr float c0 = tap(R, 0);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
+        const int64_t i = ((z + R) * ny + y) * P + x;      // field buffer index
+        const int64_t s = AXIS == 0 ? 1 : (AXIS == 1 ? P : ny * P);
+        const int64_t ia = AXIS == 0 ? x : (AXIS == 1 ? y : prm.gz0 + z);
+        const int64_t na = AXIS == 0 ? nx : (AXIS == 1 ? ny : prm.nzg);
+        float v = 0.f;
+        if (ia >= R && ia < na - R) {
+            v = __fmul_rn(c0, prm.p[i]);
+#pragma unroll
+            for (int m = 1; m <= R; ++m) v = __fmaf_rn(tap(R, m), __fadd_rn(prm.p[i - m * s], prm.p[i + m * s]), v);
+        }
+        out[(z * ny + y) * P + x] = v;
+    }
+}
+
+template <int R, int NDIM>
+__global__ void time_update_kernel(const StepParams prm, const float *__restrict__ pxx,
+                                   const float *__restrict__ pyy, const float *__restrict__ pzz) {
+    const int64_t nx = prm.nx, ny = prm.ny, P = prm.pitch;
+    const int64_t npl = nx * ny, total = npl * prm.nz;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
+        const int64_t ik = (z * ny + y) * P + x;
+        const int64_t i = ((z + R) * ny + y) * P + x;
+        float S = pxx[ik];
+        if (NDIM == 3) S = __fadd_rn(S, pyy[ik]);
+        S = __fadd_rn(S, pzz[ik]);
+        prm.pnext[i] = __fmaf_rn(prm.K[ik], S, __fmaf_rn(2.f, prm.p[i], -prm.pnext[i]));
+    }
+}
+
 // receivers of the naive path: trace_row[id] = p_next at (z, y, x) (raw, before injection)
 template <int R>
 __global__ void gather_receivers_kernel(const StepParams prm) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= prm.nrec_local) return;
     const int64_t i = ((int64_t)(prm.rec.z[j] + R) * prm.ny + prm.rec.y[j]) * prm.pitch + prm.rec.x[j];
-    prm.trace_row[prm.rec.id[j]] = prm.pnext[i];
+    trace_row_of(prm, step_index(prm))[prm.rec.id[j]] = prm.pnext[i];
 }
+
+// graph bookkeeping: the device step counter
+__global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
+__global__ void advance_step_kernel(int64_t *kdev, int64_t n) { *kdev += n; }
 
 // add_source on a field buffer, registration order; records the raw values.
 // field = buffer base; sources with sz outside [0, nz) are skipped (other slab).
 template <int R>
 __global__ void inject_kernel(float *field, const StepParams prm) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const float *wn = w_next_of(prm, step_index(prm));
     for (int s = 0; s < prm.nsrc; ++s) {
         if (prm.sz[s] < 0 || prm.sz[s] >= prm.nz) continue;
         const int64_t i = ((int64_t)(prm.sz[s] + R) * prm.ny + prm.sy[s]) * prm.pitch + prm.sx[s];
         const float v = field[i];
         prm.src_raw[s] = v;
-        field[i] = __fadd_rn(v, prm.w[s]);
+        field[i] = __fadd_rn(v, wn[s]);
     }
 }
 

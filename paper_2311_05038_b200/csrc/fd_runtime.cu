@@ -83,12 +83,12 @@ static PFN_encodeTiled get_encode() {
 // 3D fp32 tensor map over a pitched field: dims (nx, ny, planes), box (bx, by, 1);
 // out-of-bounds elements (x < 0, x >= nx, y < 0, y >= ny) are filled with zeros.
 static bool make_map(CUtensorMap *m, const float *base, int64_t nx, int64_t ny, int64_t planes, int64_t pitch,
-                     int bx, int by) {
+                     int bx, int by, int bz = 1) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)(pitch * 4), (cuuint64_t)(pitch * ny * 4)};
-    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)base, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -103,6 +103,7 @@ typedef void (*launch_fused_t)(dim3, int, cudaStream_t, const CUtensorMap &, con
 struct TileCfg {
     int ndim, r, tx, ty, ny, dp, dk;
     int pbw, tbw;        // TMA box widths (halo'd p row piece, p_prev/K row piece)
+    int pbz, tbz;        // TMA box depths in z (2D row blocks; 1 in 3D)
     int threads, smem;
     const void *kernel;
     launch_fused_t launch;
@@ -117,20 +118,39 @@ static void launch_fused(dim3 grid, int smem, cudaStream_t st, const CUtensorMap
 template <int R, int NDIM, int TX, int TY, int NY, int DP, int DK>
 static TileCfg make_cfg() {
     using C = Cfg<R, NDIM, TX, TY, NY, DP, DK>;
-    return TileCfg{NDIM, R, TX, TY, NY, DP, DK, C::PBW, C::TBW, C::NTHREADS, C::SMEM_BYTES,
+    return TileCfg{NDIM, R, TX, TY, NY, DP, DK, C::PBW, C::TBW, 1, 1, C::NTHREADS, C::SMEM_BYTES,
                    (const void *)fused_step_kernel<C>, launch_fused<C>};
 }
 
-// Compiled tiles.  3D: 4 x-y tiles per r (rows per thread 4 for r <= 2, 2 above,
-// to bound the register queue); 2D: row strips of 256/512/1024 columns.
+template <class C>
+static void launch_tile2d(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
+                          const CUtensorMap &c, const StepParams &p) {
+    tile2d_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
+}
+
+template <int R, int TX, int TY, int NY, int NS>
+static TileCfg make_cfg2() {
+    using C = Cfg2<R, TX, TY, NY, NS>;
+    return TileCfg{2, R, TX, TY, NY, NS, 0, C::PBW, C::TBW, C::PBZ, C::TBZ, C::NTHREADS, C::SMEM_BYTES,
+                   (const void *)tile2d_step_kernel<C>, launch_tile2d<C>};
+}
+
+// Compiled tiles (index = position in this table; FD_OPT_TILE selects one).
+// 3D (fused_step_kernel): x-y tiles with rows per thread NY (4 for r <= 2, 2
+// or 1 above, to bound the register queue), p-ring prefetch DP, (p_prev, K)
+// ring prefetch DK.  2D (tile2d_step_kernel): TX columns x TY-row blocks, NS
+// ring slots.  scripts/tune.py sweeps them; choose_tile() encodes the result.
 #define CFG3(R, NY) make_cfg<R, 3, 64, 32, NY, 2, 2>(), make_cfg<R, 3, 128, 32, NY, 2, 2>(), \
-                    make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2>()
-#define CFG3W(R, NY) make_cfg<R, 3, 64, 32, NY, 2, 2>(), make_cfg<R, 3, 32, 32, NY, 2, 2>(), \
-                     make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2>()
-#define CFG2(R) make_cfg<R, 2, 256, 1, 1, 6, 6>(), make_cfg<R, 2, 512, 1, 1, 6, 6>(), \
-                make_cfg<R, 2, 1024, 1, 1, 4, 4>()
+                    make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2>(), \
+                    make_cfg<R, 3, 64, 32, NY, 1, 1>(), make_cfg<R, 3, 32, 32, NY, 2, 2>()
+#define CFG3W(R) make_cfg<R, 3, 64, 32, 2, 2, 2>(), make_cfg<R, 3, 32, 32, 2, 2, 2>(), \
+                 make_cfg<R, 3, 64, 16, 2, 2, 2>(), make_cfg<R, 3, 128, 16, 2, 2, 2>(), \
+                 make_cfg<R, 3, 64, 16, 1, 2, 2>(), make_cfg<R, 3, 64, 16, 2, 1, 1>()
+#define CFG2(R) make_cfg2<R, 128, 32, 4, 3>(), make_cfg2<R, 128, 16, 4, 4>(), \
+                make_cfg2<R, 64, 32, 4, 4>(), make_cfg2<R, 128, 64, 8, 2>(), \
+                make_cfg2<R, 64, 16, 2, 4>(), make_cfg2<R, 64, 32, 4, 3>(), make_cfg2<R, 64, 32, 2, 3>()
 static const std::vector<TileCfg> &tile_table() {
-    static const std::vector<TileCfg> t = {CFG3(1, 4), CFG3(2, 4), CFG3W(3, 2), CFG3W(4, 2),
+    static const std::vector<TileCfg> t = {CFG3(1, 4), CFG3(2, 4), CFG3W(3), CFG3W(4),
                                            CFG2(1),    CFG2(2),    CFG2(3),    CFG2(4)};
     return t;
 }
@@ -205,6 +225,7 @@ struct Region {
 struct Slab {
     int64_t z0 = 0, z1 = 0, nz = 0;
     float *A = nullptr, *B = nullptr, *K = nullptr;
+    float *D[3] = {nullptr, nullptr, nullptr};   // Pxx, Pyy, Pzz (unfused decomposition only)
     float *d_src_raw = nullptr;
     CUtensorMap mA_halo, mB_halo, mA_tile, mB_tile, mK;
     std::vector<Region> regions;
@@ -229,16 +250,34 @@ struct fd_ctx {
     std::vector<SourceDef> src;
     std::vector<RecDef> rec;
     std::vector<Slab> slabs;
-    std::vector<float> vel_host;          // kept until the slabs are built (VSLABS)
     float *d_traces = nullptr;            // step-major [trace_cap][nrec]
     int64_t trace_cap = 0;
+    float *d_wtab = nullptr;              // [wcap][nsrc]: w_j of source s (fp32 of the fp64 Ricker)
+    int64_t wcap = 0;
+    int64_t *d_k = nullptr;               // device step counter (graph replays)
+    cudaStream_t own_stream = nullptr;    // used when no stream was set (capturable)
+    // CUDA graphs of G steps (one per starting buffer parity), re-captured when
+    // the trace / wavelet tables move
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    const void *gkey[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    int64_t glaunches = 0;
+    bool capturing = false;
+    int64_t gk0 = 0;
     // distributed
     ncclComm_t comm = nullptr;
     ncclUniqueId nccl_id;
     bool have_id = false;
     // kernel configuration
     int opt_kernel = 0, opt_tile = -1, opt_zchunks = 0, opt_async = 0, opt_graph = 1, opt_vslabs = 1;
+    int opt_profile = 0;
+    bool overlap = false;                 // boundary/interior split on two streams
     int tile = -1, occ = 0, nsm = 148;
+    // FD_OPT_PROFILE: CUDA events around every launch, folded into per-kernel sums
+    struct Rec { int kid; cudaEvent_t a, b; };
+    std::vector<Rec> ev_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double kms[FD_K_COUNT] = {0};
+    int64_t kcnt[FD_K_COUNT] = {0};
     double dev_bytes = 0;
 };
 
@@ -276,18 +315,32 @@ static fd_status partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_
 }
 
 static void free_slab(Slab &s) {
+    for (auto &d : s.D) { dev_free(d); d = nullptr; }
     dev_free(s.A); dev_free(s.B); dev_free(s.K); dev_free(s.d_src_raw);
     s.A = s.B = s.K = s.d_src_raw = nullptr;
     for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
 }
 
+static void drop_graphs(fd_ctx *c) {
+    for (auto &g : c->gexec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
 static void destroy_all(fd_ctx *c) {
+    drop_graphs(c);
     for (auto &s : c->slabs) free_slab(s);
     dev_free(c->d_traces);
-    c->d_traces = nullptr;
+    dev_free(c->d_wtab);
+    dev_free(c->d_k);
+    c->d_traces = nullptr; c->d_wtab = nullptr; c->d_k = nullptr;
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    c->own_stream = nullptr;
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     c->comm = nullptr;
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    for (auto &r : c->ev_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    c->ev_pending.clear(); c->ev_pool.clear();
     if (c->ev_step) cudaEventDestroy(c->ev_step);
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     c->comm_stream = nullptr; c->ev_step = c->ev_comm = nullptr;
@@ -317,8 +370,9 @@ static void compute_K(const fd_ctx *c, const float *v, int64_t nz, std::vector<f
     for (auto &t : th) t.join();
 }
 
-// Allocate a slab's buffers and upload its K (v holds the slab's planes).
-static fd_status build_slab(fd_ctx *c, Slab &s, const float *v) {
+// Allocate a slab's buffers and upload its K: from host velocities v (the
+// slab's planes), or -- when v is NULL -- copied from device K planes kdev.
+static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdev = nullptr) {
     const size_t fbytes = (size_t)buf_floats(c, s) * 4;
     const size_t kbytes = (size_t)(s.nz * plane_floats(c)) * 4;
     s.A = (float *)dev_alloc(fbytes);
@@ -328,9 +382,13 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v) {
     if (!s.A || !s.B || !s.K || !s.d_src_raw)
         return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
     c->dev_bytes += 2.0 * fbytes + kbytes;
-    std::vector<float> Kh;
-    compute_K(c, v, s.nz, Kh);
-    CUDA_TRY(c, cudaMemcpy(s.K, Kh.data(), kbytes, cudaMemcpyHostToDevice));
+    if (v) {
+        std::vector<float> Kh;
+        compute_K(c, v, s.nz, Kh);
+        CUDA_TRY(c, cudaMemcpy(s.K, Kh.data(), kbytes, cudaMemcpyHostToDevice));
+    } else {
+        CUDA_TRY(c, cudaMemcpy(s.K, kdev, kbytes, cudaMemcpyDeviceToDevice));
+    }
     CUDA_TRY(c, cudaMemset(s.A, 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.B, 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.d_src_raw, 0, kMaxSources * 4));
@@ -369,11 +427,30 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     const int64_t nloc = nz * plane;
     // validate velocity and the CFL condition (R#8) on host metadata first
     double vmax = 0;
-    for (int64_t i = 0; i < nloc; ++i) {
-        const float v = vloc[i];
-        if (!(v > 0.f) || !std::isfinite(v))
-            return fail(FD_ERR_ARG, "velocity[%lld] = %g is not finite and > 0", (long long)i, (double)v);
-        vmax = std::max(vmax, (double)v);
+    {
+        // threaded scan: max(v) and the first invalid entry
+        int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
+        nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, nloc / (1 << 20) + 1));
+        std::vector<float> vm((size_t)nt, 0.f);
+        std::vector<int64_t> bad((size_t)nt, -1);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                const int64_t a = nloc * t / nt, b = nloc * (t + 1) / nt;
+                float m = 0.f;
+                for (int64_t i = a; i < b; ++i) {
+                    const float v = vloc[i];
+                    if (!(v > 0.f) || !std::isfinite(v)) { bad[t] = i; return; }
+                    m = std::max(m, v);
+                }
+                vm[t] = m;
+            });
+        for (auto &x : th) x.join();
+        for (int t = 0; t < nt; ++t)
+            if (bad[t] >= 0)
+                return fail(FD_ERR_ARG, "velocity[%lld] = %g is not finite and > 0", (long long)bad[t],
+                            (double)vloc[bad[t]]);
+        for (int t = 0; t < nt; ++t) vmax = std::max(vmax, (double)vm[t]);
     }
     const double ratio = vmax * dt / h, lim = cfl_limit(ndim, R);
     if (!(flags & FD_FLAG_ALLOW_UNSTABLE) && ratio > lim)
@@ -406,7 +483,6 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     Slab &s = c->slabs[0];
     s.z0 = z0; s.z1 = z1; s.nz = nz;
     fd_status st = build_slab(c, s, vloc);
-    if (st == FD_OK && nranks == 1) c->vel_host.assign(vloc, vloc + nloc);
     if (st == FD_OK) {
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) st = fail(FD_ERR_CUDA, "device setup failed: %s", cudaGetErrorString(e));
@@ -445,7 +521,10 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     if (c->opt_zchunks > 0) return (int)std::min<int64_t>(c->opt_zchunks, std::max<int64_t>(1, span));
     const int64_t slots = (int64_t)c->nsm * occ, ntiles = ntiles_of(c, t);
     int64_t ch = std::max<int64_t>(1, slots / ntiles);
-    ch = std::min<int64_t>(ch, std::max<int64_t>(1, span / std::max(4 * c->R, 8)));
+    // 3D: chunks of >= max(4r, 8) planes (the 2r warm-up planes stay small);
+    // 2D: >= 2 row blocks per chunk
+    const int64_t minp = c->ndim == 3 ? std::max(4 * c->R, 8) : 2 * t.ty;
+    ch = std::min<int64_t>(ch, std::max<int64_t>(1, span / minp));
     return (int)ch;
 }
 
@@ -466,8 +545,8 @@ static void choose_tile(fd_ctx *c, int64_t span) {
         const int64_t units = ntiles_of(c, t) * chunks;
         const int64_t waves = (units + slots - 1) / slots;
         const double fill = (double)units / (double)(waves * slots);
-        const double halo = (double)(t.tx + 8) * (t.ty + (c->ndim == 3 ? 2 * c->R : 0)) / ((double)t.tx * t.ty);
-        const double warm = (double)(2 * c->R * chunks) / (double)span;
+        const double halo = (double)(t.tx + 8) * (t.ty + 2 * c->R) / ((double)t.tx * t.ty);
+        const double warm = c->ndim == 3 ? (double)(2 * c->R * chunks) / (double)span : 0.0;
         const double bytes = 12.0 + 4.0 * (halo + warm);
         const double score = fill * 16.0 / bytes;
         if (score > best) { best = score; bi = i; bocc = occ; }
@@ -479,12 +558,14 @@ static void choose_tile(fd_ctx *c, int64_t span) {
 static fd_status make_maps(fd_ctx *c, Slab &s) {
     const TileCfg &t = tile_table()[c->tile];
     const int64_t planes = s.nz + 2 * c->R;
+    // 3D: boxes (x, y) of one plane; 2D: boxes of pbz / tbz rows (nyg = 1)
     const int hy = c->ndim == 3 ? c->R : 0;
-    bool ok = make_map(&s.mA_halo, s.A, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
-              make_map(&s.mB_halo, s.B, c->nxg, c->nyg, planes, c->pitch, t.pbw, t.ty + 2 * hy) &&
-              make_map(&s.mA_tile, s.A, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
-              make_map(&s.mB_tile, s.B, c->nxg, c->nyg, planes, c->pitch, t.tbw, t.ty) &&
-              make_map(&s.mK, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, t.ty);
+    const int pby = c->ndim == 3 ? t.ty + 2 * hy : 1, tby = c->ndim == 3 ? t.ty : 1;
+    bool ok = make_map(&s.mA_halo, s.A, c->nxg, c->nyg, planes, c->pitch, t.pbw, pby, t.pbz) &&
+              make_map(&s.mB_halo, s.B, c->nxg, c->nyg, planes, c->pitch, t.pbw, pby, t.pbz) &&
+              make_map(&s.mA_tile, s.A, c->nxg, c->nyg, planes, c->pitch, t.tbw, tby, t.tbz) &&
+              make_map(&s.mB_tile, s.B, c->nxg, c->nyg, planes, c->pitch, t.tbw, tby, t.tbz) &&
+              make_map(&s.mK, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, tby, t.tbz);
     if (!ok) {
         c->poisoned = true;
         return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -499,7 +580,7 @@ static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g) {
     g.d_rec = nullptr;
     struct L { int32_t unit, z, y, x, id; };
     std::vector<L> loc;
-    const TileCfg *t = (c->opt_kernel == 1) ? nullptr : &tile_table()[c->tile];
+    const TileCfg *t = (c->opt_kernel != 0) ? nullptr : &tile_table()[c->tile];
     int ntx = 1, ntiles = 1;
     if (t) {
         ntx = (int)((c->nxg + t->tx - 1) / t->tx);
@@ -511,10 +592,16 @@ static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g) {
         if (lz < g.zlo || lz >= g.zhi) continue;
         L l{0, (int32_t)lz, (int32_t)c->rec[j].g[1], (int32_t)c->rec[j].g[2], (int32_t)j};
         if (t) {
+            // the chunk containing plane lz, as the kernels split [zlo, zhi):
+            // 3D by planes, 2D by whole blocks of ty rows
             int ch = 0;
-            for (int q = 0; q < g.zchunks; ++q)
-                if (g.zlo + (span * q) / g.zchunks <= lz) ch = q;
-            l.unit = ch * ntiles + (l.y / t->ty) * ntx + (l.x / t->tx);
+            const int64_t nb = (span + t->ty - 1) / t->ty;
+            for (int q = 0; q < g.zchunks; ++q) {
+                const int64_t first = c->ndim == 3 ? g.zlo + (span * q) / g.zchunks
+                                                   : g.zlo + ((nb * q) / g.zchunks) * t->ty;
+                if (first <= lz) ch = q;
+            }
+            l.unit = ch * ntiles + (c->ndim == 3 ? (l.y / t->ty) * ntx : 0) + (l.x / t->tx);
         }
         loc.push_back(l);
     }
@@ -545,47 +632,69 @@ static fd_status split_virtual(fd_ctx *c, int n) {
     if (c->nranks > 1) return fail(FD_ERR_STATE, "FD_OPT_VSLABS is for single-process contexts");
     const int64_t nz = c->z1 - c->z0;
     if (nz < (int64_t)n * 2 * c->R) return fail(FD_ERR_ARG, "too many virtual slabs for nz=%lld", (long long)nz);
-    // keep the current fields (fd_set_wavefield may have set them)
+    // the new slabs take their planes of K and of both fields (fd_set_wavefield
+    // may have set them) from the single slab by device copies
     const int64_t pf = plane_floats(c);
-    std::vector<float> hA((size_t)(nz * pf)), hB((size_t)(nz * pf)), raw(kMaxSources);
-    Slab &o = c->slabs[0];
-    CUDA_TRY(c, cudaMemcpy(hA.data(), o.A + c->R * pf, hA.size() * 4, cudaMemcpyDeviceToHost));
-    CUDA_TRY(c, cudaMemcpy(hB.data(), o.B + c->R * pf, hB.size() * 4, cudaMemcpyDeviceToHost));
+    Slab o = c->slabs[0];
+    std::vector<Slab> ns((size_t)n);
     c->dev_bytes = 0;
-    free_slab(o);
-    c->slabs.assign(n, Slab());
-    const int64_t plane = c->nyg * c->nxg;
-    for (int q = 0; q < n; ++q) {
-        Slab &s = c->slabs[q];
+    fd_status st = FD_OK;
+    for (int q = 0; q < n && st == FD_OK; ++q) {
+        Slab &s = ns[q];
         int64_t a, b;
         partition(nz, n, q, &a, &b);
         s.z0 = c->z0 + a; s.z1 = c->z0 + b; s.nz = b - a;
-        fd_status st = build_slab(c, s, c->vel_host.data() + a * plane);
-        if (st) return st;
-        CUDA_TRY(c, cudaMemcpy(s.A + c->R * pf, hA.data() + a * pf, (size_t)(s.nz * pf) * 4, cudaMemcpyHostToDevice));
-        CUDA_TRY(c, cudaMemcpy(s.B + c->R * pf, hB.data() + a * pf, (size_t)(s.nz * pf) * 4, cudaMemcpyHostToDevice));
+        st = build_slab(c, s, nullptr, o.K + a * pf);
+        if (st) break;
+        const size_t bytes = (size_t)(s.nz * pf) * 4;
+        CUDA_TRY(c, cudaMemcpy(s.A + c->R * pf, o.A + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
+        CUDA_TRY(c, cudaMemcpy(s.B + c->R * pf, o.B + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
     }
-    return FD_OK;
+    free_slab(o);
+    c->slabs.swap(ns);
+    return st;
 }
 
 static fd_status prepare(fd_ctx *c) {
     fd_status st = split_virtual(c, c->opt_vslabs);
     if (st) return st;
-    c->vel_host.clear();
-    c->vel_host.shrink_to_fit();
+    if (!c->stream) {
+        // no stream set: an own non-blocking stream (capturable for graphs)
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+    }
+    c->d_k = (int64_t *)dev_alloc(sizeof(int64_t));
+    if (!c->d_k) return fail(FD_ERR_NOMEM, "step counter allocation failed");
     int64_t maxnz = 0;
     for (auto &s : c->slabs) maxnz = std::max(maxnz, s.nz);
-    if (c->opt_kernel != 1) {
+    if (c->opt_kernel == 0) {
         choose_tile(c, maxnz);
         if (c->tile < 0) return fail(FD_ERR_CUDA, "no fused kernel configuration fits this device");
         const TileCfg &t = tile_table()[c->tile];
         CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
     }
-    const bool dist = c->nranks > 1;
-    for (auto &s : c->slabs) {
-        if (c->opt_kernel != 1) {
+    // overlapped schedule (boundary planes + exchange on the comm stream,
+    // interior on the user stream): NCCL ranks, and virtual slabs, which run
+    // the identical schedule with device-copy halos
+    const bool overlap = (c->nranks > 1 || c->slabs.size() > 1) && c->opt_kernel == 0;
+    c->overlap = overlap;
+    for (size_t q = 0; q < c->slabs.size(); ++q) {
+        Slab &s = c->slabs[q];
+        const bool has_lo = c->nranks > 1 ? c->rank > 0 : q > 0;
+        const bool has_hi = c->nranks > 1 ? c->rank < c->nranks - 1 : q + 1 < c->slabs.size();
+        if (c->opt_kernel == 0) {
             st = make_maps(c, s);
             if (st) return st;
+        }
+        if (c->opt_kernel == 3) {
+            // derivative fields of the unfused decomposition (pitched like K)
+            const size_t db = (size_t)(s.nz * plane_floats(c)) * 4;
+            for (int a = 0; a < 3; ++a) {
+                if (a == 1 && c->ndim == 2) continue;
+                s.D[a] = (float *)dev_alloc(db);
+                if (!s.D[a]) return fail(FD_ERR_NOMEM, "derivative field allocation failed");
+                c->dev_bytes += (double)db;
+            }
         }
         s.regions.clear();
         const int32_t nz = (int32_t)s.nz, R = c->R;
@@ -593,15 +702,15 @@ static fd_status prepare(fd_ctx *c) {
             if (hi <= lo) return;
             Region g;
             g.zlo = lo; g.zhi = hi; g.boundary = boundary;
-            g.zchunks = (c->opt_kernel == 1) ? 1 : chunks_for(c, tile_table()[c->tile], c->occ, hi - lo);
+            g.zchunks = (c->opt_kernel != 0) ? 1 : chunks_for(c, tile_table()[c->tile], c->occ, hi - lo);
             s.regions.push_back(g);
         };
-        if (dist && c->opt_kernel != 1) {
+        if (overlap) {
             // boundary planes first (they feed the exchange), interior overlaps it
-            const int32_t lo_end = c->rank > 0 ? R : 0;
-            const int32_t hi_beg = c->rank < c->nranks - 1 ? nz - R : nz;
-            if (c->rank > 0) add(0, R, true);
-            if (c->rank < c->nranks - 1) add(nz - R, nz, true);
+            const int32_t lo_end = has_lo ? R : 0;
+            const int32_t hi_beg = has_hi ? nz - R : nz;
+            if (has_lo) add(0, R, true);
+            if (has_hi) add(nz - R, nz, true);
             add(lo_end, hi_beg, false);
         } else {
             add(0, nz, false);
@@ -611,12 +720,14 @@ static fd_status prepare(fd_ctx *c) {
             if (st) return st;
         }
     }
-    if (dist) {
+    if (overlap) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         CUDA_TRY(c, cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+    }
+    if (c->nranks > 1) {
         ncclResult_t r = nccl().CommInitRank(&c->comm, c->nranks, c->nccl_id, c->rank);
         if (r != 0) {
             c->poisoned = true;
@@ -626,23 +737,38 @@ static fd_status prepare(fd_ctx *c) {
     return FD_OK;
 }
 
-static fd_status ensure_traces(fd_ctx *c, int64_t steps_needed) {
-    const int64_t nrec = (int64_t)c->rec.size();
-    if (nrec == 0 || steps_needed <= c->trace_cap) return FD_OK;
-    int64_t cap = std::max<int64_t>(steps_needed, 2 * c->trace_cap);
-    cap = std::max<int64_t>(cap, 16);
-    float *nb = (float *)dev_alloc((size_t)(cap * nrec) * 4);
-    if (!nb) return fail(FD_ERR_NOMEM, "trace buffer allocation failed");
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(nb, 0, (size_t)(cap * nrec) * 4, c->stream));
-    if (c->d_traces) {
-        CUDA_TRY(c, cudaMemcpyAsync(nb, c->d_traces, (size_t)(c->trace_cap * nrec) * 4, cudaMemcpyDeviceToDevice,
-                                    c->stream));
+// Grow the step-indexed device tables to cover steps [0, steps_needed):
+// traces (rows 0..steps_needed-1) and the wavelet table (w_0..w_steps_needed,
+// the last step injects w_{k+1}).  Doubling growth; moves invalidate graphs.
+static fd_status ensure_tables(fd_ctx *c, int64_t steps_needed) {
+    const int64_t nrec = (int64_t)c->rec.size(), nsrc = (int64_t)c->src.size();
+    if (nrec > 0 && steps_needed > c->trace_cap) {
+        int64_t cap = std::max<int64_t>({steps_needed, 2 * c->trace_cap, 16});
+        float *nb = (float *)dev_alloc((size_t)(cap * nrec) * 4);
+        if (!nb) return fail(FD_ERR_NOMEM, "trace buffer allocation failed");
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-        dev_free(c->d_traces);
+        CUDA_TRY(c, cudaMemset(nb, 0, (size_t)(cap * nrec) * 4));
+        if (c->d_traces) {
+            CUDA_TRY(c, cudaMemcpy(nb, c->d_traces, (size_t)(c->trace_cap * nrec) * 4, cudaMemcpyDeviceToDevice));
+            dev_free(c->d_traces);
+        }
+        c->d_traces = nb;
+        c->trace_cap = cap;
     }
-    c->d_traces = nb;
-    c->trace_cap = cap;
+    if (steps_needed + 1 > c->wcap) {
+        int64_t cap = std::max<int64_t>({steps_needed + 1, 2 * c->wcap, 16});
+        std::vector<float> h((size_t)(cap * std::max<int64_t>(nsrc, 1)), 0.f);
+        for (int64_t j = 0; j < cap; ++j)
+            for (int64_t q = 0; q < nsrc; ++q)
+                h[j * nsrc + q] = (float)(c->src[q].amp * ricker((double)j * c->dt, c->src[q].f, c->src[q].t0));
+        float *nb = (float *)dev_alloc(h.size() * 4);
+        if (!nb) return fail(FD_ERR_NOMEM, "wavelet table allocation failed");
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        CUDA_TRY(c, cudaMemcpy(nb, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        dev_free(c->d_wtab);
+        c->d_wtab = nb;
+        c->wcap = cap;
+    }
     return FD_OK;
 }
 
@@ -659,9 +785,8 @@ static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepPar
         p.sz[q] = (int32_t)(c->src[q].g[0] - s.z0);
         p.sy[q] = (int32_t)c->src[q].g[1];
         p.sx[q] = (int32_t)c->src[q].g[2];
-        // w_{k+1}: the value injected into P^{k+1} by this launch (eager form)
-        p.w[q] = (float)(c->src[q].amp * ricker((double)(step_k + 1) * c->dt, c->src[q].f, c->src[q].t0));
     }
+    p.wtab = c->d_wtab;
     p.src_raw = s.d_src_raw;
     if (g && g->d_rec) {
         const int n = g->nrec;
@@ -669,10 +794,47 @@ static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepPar
         p.rec.y = g->d_rec + n;
         p.rec.x = g->d_rec + 2 * n;
         p.rec.id = g->d_rec + 3 * n;
-        p.rec.off = (c->opt_kernel == 1) ? nullptr : g->d_rec + 4 * n;
+        p.rec.off = (c->opt_kernel != 0) ? nullptr : g->d_rec + 4 * n;
         p.nrec_local = n;
     }
-    p.trace_row = (c->d_traces && step_k >= 0) ? c->d_traces + step_k * (int64_t)c->rec.size() : nullptr;
+    p.traces = c->d_traces;
+    p.nrec_total = (int32_t)c->rec.size();
+    // step index: baked (plain launches) or *d_k + offset (graph capture)
+    p.k = step_k;
+    if (c->capturing) { p.kdev = c->d_k; p.koff = (int32_t)(step_k - c->gk0); }
+}
+
+static cudaEvent_t pool_event(fd_ctx *c) {
+    if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Run `launch` on stream st; with FD_OPT_PROFILE, bracket it with events.
+template <class F>
+static void tracked(fd_ctx *c, int kid, cudaStream_t st, F &&launch, bool is_kernel = true) {
+    if (is_kernel) ++c->launches;
+    if (!c->opt_profile) { launch(); return; }
+    cudaEvent_t a = pool_event(c), b = pool_event(c);
+    cudaEventRecord(a, st);
+    launch();
+    cudaEventRecord(b, st);
+    c->ev_pending.push_back({kid, a, b});
+}
+
+static fd_status fold_times(fd_ctx *c) {
+    for (auto &r : c->ev_pending) {
+        CUDA_TRY(c, cudaEventSynchronize(r.b));
+        float ms = 0;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, r.a, r.b));
+        c->kms[r.kid] += ms;
+        c->kcnt[r.kid] += 1;
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->ev_pending.clear();
+    return FD_OK;
 }
 
 template <int R> static void launch_inject(cudaStream_t st, float *field, const StepParams &p) {
@@ -689,13 +851,26 @@ template <int R> static void launch_gather(cudaStream_t st, int n, const StepPar
 }
 
 static void dispatch_inject(fd_ctx *c, cudaStream_t st, float *field, const StepParams &p) {
-    switch (c->R) {
-    case 1: launch_inject<1>(st, field, p); break;
-    case 2: launch_inject<2>(st, field, p); break;
-    case 3: launch_inject<3>(st, field, p); break;
-    default: launch_inject<4>(st, field, p); break;
-    }
-    ++c->launches;
+    tracked(c, FD_K_INJECT, st, [&] {
+        switch (c->R) {
+        case 1: launch_inject<1>(st, field, p); break;
+        case 2: launch_inject<2>(st, field, p); break;
+        case 3: launch_inject<3>(st, field, p); break;
+        default: launch_inject<4>(st, field, p); break;
+        }
+    });
+}
+
+template <int R, int NDIM>
+static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStream_t st, const StepParams &p) {
+    const int64_t total = c->nxg * c->nyg * s.nz;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    // Listing 3 order: fd_pzz, [fd_pyy], fd_pxx, fd_time
+    tracked(cm, FD_K_PZZ, st, [&] { d2_axis_kernel<R, 2><<<blocks, 256, 0, st>>>(p, s.D[2]); });
+    if (NDIM == 3) tracked(cm, FD_K_PYY, st, [&] { d2_axis_kernel<R, 1><<<blocks, 256, 0, st>>>(p, s.D[1]); });
+    tracked(cm, FD_K_PXX, st, [&] { d2_axis_kernel<R, 0><<<blocks, 256, 0, st>>>(p, s.D[0]); });
+    tracked(cm, FD_K_TIME, st,
+            [&] { time_update_kernel<R, NDIM><<<blocks, 256, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });
 }
 
 static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
@@ -705,27 +880,43 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     p.pnext = prev;
     p.p = cur;
     p.K = s.K;
-    if (c->opt_kernel == 1) {
-        // naive path: stencil, receivers, injection (three launches)
-        switch (c->R * 10 + c->ndim) {
-        case 12: launch_naive<1, 2>(c, s, st, p); break;
-        case 13: launch_naive<1, 3>(c, s, st, p); break;
-        case 22: launch_naive<2, 2>(c, s, st, p); break;
-        case 23: launch_naive<2, 3>(c, s, st, p); break;
-        case 32: launch_naive<3, 2>(c, s, st, p); break;
-        case 33: launch_naive<3, 3>(c, s, st, p); break;
-        case 42: launch_naive<4, 2>(c, s, st, p); break;
-        default: launch_naive<4, 3>(c, s, st, p); break;
-        }
-        ++c->launches;
-        if (g.nrec > 0) {
-            switch (c->R) {
-            case 1: launch_gather<1>(st, g.nrec, p); break;
-            case 2: launch_gather<2>(st, g.nrec, p); break;
-            case 3: launch_gather<3>(st, g.nrec, p); break;
-            default: launch_gather<4>(st, g.nrec, p); break;
+    if (c->opt_kernel == 1 || c->opt_kernel == 3) {
+        // reference paths: naive fused stencil (1) or the paper's unfused
+        // decomposition (3); then receivers and injection as separate launches
+        if (c->opt_kernel == 1) {
+            tracked(c, FD_K_NAIVE, st, [&] {
+                switch (c->R * 10 + c->ndim) {
+                case 12: launch_naive<1, 2>(c, s, st, p); break;
+                case 13: launch_naive<1, 3>(c, s, st, p); break;
+                case 22: launch_naive<2, 2>(c, s, st, p); break;
+                case 23: launch_naive<2, 3>(c, s, st, p); break;
+                case 32: launch_naive<3, 2>(c, s, st, p); break;
+                case 33: launch_naive<3, 3>(c, s, st, p); break;
+                case 42: launch_naive<4, 2>(c, s, st, p); break;
+                default: launch_naive<4, 3>(c, s, st, p); break;
+                }
+            });
+        } else {
+            switch (c->R * 10 + c->ndim) {
+            case 12: launch_unfused<1, 2>(c, c, s, st, p); break;
+            case 13: launch_unfused<1, 3>(c, c, s, st, p); break;
+            case 22: launch_unfused<2, 2>(c, c, s, st, p); break;
+            case 23: launch_unfused<2, 3>(c, c, s, st, p); break;
+            case 32: launch_unfused<3, 2>(c, c, s, st, p); break;
+            case 33: launch_unfused<3, 3>(c, c, s, st, p); break;
+            case 42: launch_unfused<4, 2>(c, c, s, st, p); break;
+            default: launch_unfused<4, 3>(c, c, s, st, p); break;
             }
-            ++c->launches;
+        }
+        if (g.nrec > 0) {
+            tracked(c, FD_K_GATHER, st, [&] {
+                switch (c->R) {
+                case 1: launch_gather<1>(st, g.nrec, p); break;
+                case 2: launch_gather<2>(st, g.nrec, p); break;
+                case 3: launch_gather<3>(st, g.nrec, p); break;
+                default: launch_gather<4>(st, g.nrec, p); break;
+                }
+            });
         }
         if (p.nsrc > 0) dispatch_inject(c, st, prev, p);
         return;
@@ -737,8 +928,7 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     g.ctas = (int)grid.x;
     const CUtensorMap &mp = c->cur_is_A ? s.mA_halo : s.mB_halo;
     const CUtensorMap &mpp = c->cur_is_A ? s.mB_tile : s.mA_tile;
-    t.launch(grid, t.smem, st, mp, mpp, s.mK, p);
-    ++c->launches;
+    tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
 // Halo exchange of the field that becomes P (buffer `which_next`: true = the
@@ -788,32 +978,78 @@ static fd_status exchange(fd_ctx *c, bool next, cudaStream_t st) {
 
 static fd_status one_step(fd_ctx *c) {
     fd_status s;
-    if (c->nranks > 1 && c->opt_kernel != 1) {
-        // comm stream: boundary planes -> NCCL exchange; user stream: interior.
-        // Step k+1 starts after both (its boundary kernel overwrites planes
-        // that step k's interior kernel reads as p).
-        Slab &sl = c->slabs[0];
+    if (c->overlap) {
+        // comm stream: boundary planes -> halo exchange (NCCL or device copies);
+        // user stream: interior planes.  Step k+1 starts after both (its
+        // boundary kernel overwrites planes that step k's interior kernel reads
+        // as p; its kernels read the halos received in step k).
         CUDA_TRY(c, cudaEventRecord(c->ev_step, c->stream));
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
-        for (auto &g : sl.regions)
-            if (g.boundary) launch_region(c, sl, g, c->comm_stream);
-        s = exchange(c, true, c->comm_stream);
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.regions)
+                if (g.boundary) launch_region(c, sl, g, c->comm_stream);
+        tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, true, c->comm_stream); }, false);
         if (s) return s;
         CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
-        for (auto &g : sl.regions)
-            if (!g.boundary) launch_region(c, sl, g, c->stream);
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.regions)
+                if (!g.boundary) launch_region(c, sl, g, c->stream);
         CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     } else {
         for (auto &sl : c->slabs)
             for (auto &g : sl.regions) launch_region(c, sl, g, c->stream);
         if (c->slabs.size() > 1 || c->nranks > 1) {
-            s = exchange(c, true, c->stream);
+            tracked(c, FD_K_HALO, c->stream, [&] { s = exchange(c, true, c->stream); }, false);
             if (s) return s;
         }
     }
     CUDA_TRY(c, cudaGetLastError());
     c->cur_is_A = !c->cur_is_A;
     ++c->k;
+    return FD_OK;
+}
+
+// ------------------------------------------------------------ CUDA graphs
+// kGraphSteps consecutive steps captured once per starting buffer parity and
+// replayed (launch-bound small grids).  Kernels read k = *d_k + offset; the
+// graph ends by advancing d_k.  Not used with the two-stream overlap schedule
+// or while profiling.
+constexpr int64_t kGraphSteps = 16;
+
+static bool graphs_usable(const fd_ctx *c) {
+    return c->opt_graph && !c->overlap && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream;
+}
+
+static fd_status capture_graph(fd_ctx *c, int par) {
+    const int64_t k0 = c->k, l0 = c->launches;
+    const bool a0 = c->cur_is_A;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    c->gk0 = k0;
+    fd_status s = FD_OK;
+    for (int64_t i = 0; i < kGraphSteps && s == FD_OK; ++i) s = one_step(c);
+    advance_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, kGraphSteps);
+    c->capturing = false;
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    c->glaunches = c->launches - l0 + 1;
+    c->k = k0; c->cur_is_A = a0; c->launches = l0;
+    if (s) { if (graph) cudaGraphDestroy(graph); return s; }
+    if (e != cudaSuccess || !graph) {
+        cudaGetLastError();
+        c->opt_graph = 0;                 // fall back to plain launches
+        return FD_OK;
+    }
+    e = cudaGraphInstantiate(&c->gexec[par], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->gexec[par] = nullptr;
+        c->opt_graph = 0;
+        return FD_OK;
+    }
+    c->gkey[par][0] = c->d_traces;
+    c->gkey[par][1] = c->d_wtab;
     return FD_OK;
 }
 
@@ -903,7 +1139,7 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         if (s) return s;
         c->started = true;
     }
-    s = ensure_traces(c, c->k + n);
+    s = ensure_tables(c, c->k + n);
     if (s) return s;
     if (!c->injected) {
         // add_source of step k on the current field by the owning slab;
@@ -919,7 +1155,28 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         }
         c->injected = true;
     }
-    for (int64_t i = 0; i < n; ++i) {
+    int64_t i = 0;
+    if (graphs_usable(c) && n >= kGraphSteps) {
+        // replay G-step graphs; the device counter d_k carries k
+        set_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, c->k);
+        ++c->launches;
+        for (; n - i >= kGraphSteps; i += kGraphSteps) {
+            const int par = c->cur_is_A ? 0 : 1;
+            if (c->gexec[par] && (c->gkey[par][0] != c->d_traces || c->gkey[par][1] != c->d_wtab)) {
+                cudaGraphExecDestroy(c->gexec[par]);
+                c->gexec[par] = nullptr;
+            }
+            if (!c->gexec[par]) {
+                s = capture_graph(c, par);
+                if (s) return s;
+                if (!c->gexec[par]) break;   // capture unsupported: plain launches
+            }
+            CUDA_TRY(c, cudaGraphLaunch(c->gexec[par], c->stream));
+            c->k += kGraphSteps;             // G even: buffer parity unchanged
+            c->launches += c->glaunches;
+        }
+    }
+    for (; i < n; ++i) {
         s = one_step(c);
         if (s) return s;
     }
@@ -1046,10 +1303,17 @@ fd_status fd_set_wavefield(fd_ctx *c, int which, const float *host_in) {
 fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
     fd_status s = check_ctx(c);
     if (s) return s;
-    if (c->started) return fail(FD_ERR_STATE, "options only before the first fd_step");
+    if (key == FD_OPT_ASYNC) { c->opt_async = v ? 1 : 0; return FD_OK; }
+    if (key == FD_OPT_PROFILE) {
+        s = fold_times(c);
+        if (s) return s;
+        c->opt_profile = v ? 1 : 0;
+        return FD_OK;
+    }
+    if (c->started) return fail(FD_ERR_STATE, "option %d only before the first fd_step", key);
     switch (key) {
     case FD_OPT_KERNEL:
-        if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_KERNEL must be 0, 1 or 2");
+        if (v < 0 || v > 3) return fail(FD_ERR_ARG, "FD_OPT_KERNEL must be 0, 1, 2 or 3");
         c->opt_kernel = (v == 2) ? 0 : (int)v;
         return FD_OK;
     case FD_OPT_TILE: {
@@ -1064,7 +1328,6 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         if (v < 0 || v > 4096) return fail(FD_ERR_ARG, "bad zchunks");
         c->opt_zchunks = (int)v;
         return FD_OK;
-    case FD_OPT_ASYNC: c->opt_async = v ? 1 : 0; return FD_OK;
     case FD_OPT_GRAPH: c->opt_graph = v ? 1 : 0; return FD_OK;
     case FD_OPT_VSLABS:
         if (v < 1 || v > 64) return fail(FD_ERR_ARG, "FD_OPT_VSLABS must be in [1, 64]");
@@ -1073,6 +1336,25 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         return FD_OK;
     default: return fail(FD_ERR_ARG, "unknown option %d", key);
     }
+}
+
+fd_status fd_get_kernel_times(fd_ctx *c, double *ms, int64_t *launches) {
+    fd_status s = check_ctx(c);
+    if (s) return s;
+    if (!ms || !launches) return fail(FD_ERR_ARG, "ms/launches is NULL");
+    s = fold_times(c);
+    if (s) return s;
+    for (int i = 0; i < FD_K_COUNT; ++i) { ms[i] = c->kms[i]; launches[i] = c->kcnt[i]; }
+    return FD_OK;
+}
+
+fd_status fd_reset_kernel_times(fd_ctx *c) {
+    fd_status s = check_ctx(c);
+    if (s) return s;
+    s = fold_times(c);
+    if (s) return s;
+    for (int i = 0; i < FD_K_COUNT; ++i) { c->kms[i] = 0; c->kcnt[i] = 0; }
+    return FD_OK;
 }
 
 fd_status fd_get_info(fd_ctx *c, fd_info *o) {
@@ -1089,7 +1371,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->pitch = c->pitch;
     o->order = c->order;
     o->device_bytes = c->dev_bytes;
-    if (c->opt_kernel == 1) { o->kernel = 1; return FD_OK; }
+    if (c->opt_kernel != 0) { o->kernel = c->opt_kernel; return FD_OK; }
     o->kernel = 2;
     if (!c->started) choose_tile(c, c->z1 - c->z0);
     if (c->tile >= 0) {

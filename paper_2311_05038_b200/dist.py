@@ -1,0 +1,89 @@
+"""Multi-process harness for the z-slab decomposition.
+
+One process per GPU (launched by torchrun); torch.distributed is the plumbing:
+it broadcasts the NCCL unique id from rank 0, assembles traces and gathers the
+wavefield.  The per-step halo exchange itself runs inside libfd.so (NCCL
+send/recv on the library's comm stream), never through torch.
+
+Everything here is argument marshalling and host-side assembly; it does no
+arithmetic of the method.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import fd as _fd
+
+
+def partition(nz: int, nranks: int, rank: int) -> tuple[int, int]:
+    """The owned planes [z0, z1) of a slab (same rule as the C ABI)."""
+    return _fd.fd_partition(nz, nranks, rank)
+
+
+def bootstrap_nccl_id(make_id=None) -> bytes:
+    """Rank 0 creates a 128-byte ncclUniqueId; every rank receives it."""
+    import torch.distributed as dist
+    make_id = make_id or _fd.fd_nccl_get_unique_id
+    box = [make_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    uid = box[0]
+    assert isinstance(uid, (bytes, bytearray)) and len(uid) == 128
+    return bytes(uid)
+
+
+def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *, device: int = -1,
+           nccl_id: bytes | None = None, flags: int = 0, options: dict | None = None,
+           stream: int | None = None) -> "_fd.Simulation":
+    """Create this rank's slab context; ``vel_slab`` holds only the owned planes."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if nccl_id is None and world > 1:
+        nccl_id = bootstrap_nccl_id()
+    return _fd.Simulation(vel_slab, h, dt, order, flags,
+                          dist={"global_dims": tuple(global_dims), "rank": rank, "nranks": world,
+                                "device": device, "nccl_id": nccl_id, "vel_is_slab": True},
+                          options=options, stream=stream)
+
+
+def all_ok(ok: bool) -> bool:
+    """True iff every rank reports ok (guards collective steps after a local failure)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([0 if ok else 1], dtype=torch.int32)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item()) == 0
+
+
+def assemble_traces(local: np.ndarray) -> np.ndarray:
+    """Sum the per-rank trace matrices: rows of receivers owned by other ranks
+    are exactly 0 on each rank (fd_get_traces), so the sum is exact."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(local, dtype=np.float32)).clone()
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy()
+
+
+def gather_wavefield(local: np.ndarray, dst: int = 0):
+    """Concatenate the ranks' owned planes along z on rank ``dst`` (None elsewhere)."""
+    import torch.distributed as dist
+    parts = [None] * dist.get_world_size() if dist.get_rank() == dst else None
+    dist.gather_object(np.ascontiguousarray(local), parts, dst=dst)
+    if dist.get_rank() != dst:
+        return None
+    return np.concatenate(parts, axis=0)
+
+
+def max_over_ranks(x: float) -> float:
+    """Max of a per-rank scalar (timings are reported as the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

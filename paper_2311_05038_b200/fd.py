@@ -21,12 +21,14 @@ FD_ERR_NOMEM, FD_ERR_CUDA, FD_ERR_NCCL, FD_ERR_STATE = -4, -5, -6, -7
 FD_FIELD_CUR, FD_FIELD_PREV = 0, 1
 FD_FLAG_ALLOW_UNSTABLE = 1
 FD_OPT_KERNEL, FD_OPT_TILE, FD_OPT_ZCHUNKS, FD_OPT_ASYNC, FD_OPT_GRAPH, FD_OPT_VSLABS = 1, 2, 3, 4, 5, 6
+FD_OPT_PROFILE = 7
+KERNEL_KINDS = ["fused", "naive", "gather", "inject", "fd_pxx", "fd_pyy", "fd_pzz", "fd_time", "halo"]
 
 EXPORTED = [
     "fd_create", "fd_create_dist", "fd_partition", "fd_nccl_get_unique_id", "fd_add_source",
     "fd_set_receivers", "fd_step", "fd_get_wavefield", "fd_get_traces", "fd_destroy",
     "fd_strerror", "fd_last_error", "fd_set_stream", "fd_set_allocator", "fd_set_wavefield",
-    "fd_set_option", "fd_get_info",
+    "fd_set_option", "fd_get_info", "fd_get_kernel_times", "fd_reset_kernel_times",
 ]
 
 
@@ -91,6 +93,8 @@ def _load() -> ctypes.CDLL:
         "fd_set_wavefield": ([ctypes.c_void_p, ctypes.c_int, _f32p], st),
         "fd_set_option": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int64], st),
         "fd_get_info": ([ctypes.c_void_p, ctypes.POINTER(FdInfo)], st),
+        "fd_get_kernel_times": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _i64p], st),
+        "fd_reset_kernel_times": ([ctypes.c_void_p], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -208,6 +212,18 @@ def fd_get_info(ctx) -> dict:
     return info.as_dict()
 
 
+def fd_get_kernel_times(ctx) -> dict:
+    """{kind: (ms_total, launches)} accumulated while FD_OPT_PROFILE = 1."""
+    ms = (ctypes.c_double * len(KERNEL_KINDS))()
+    n = (ctypes.c_int64 * len(KERNEL_KINDS))()
+    _check(lib.fd_get_kernel_times(ctx, ms, n), "fd_get_kernel_times")
+    return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_KINDS) if n[i]}
+
+
+def fd_reset_kernel_times(ctx):
+    _check(lib.fd_reset_kernel_times(ctx), "fd_reset_kernel_times")
+
+
 _alloc_keepalive = []
 
 
@@ -281,6 +297,12 @@ class Simulation:
 
     def info(self) -> dict:
         return fd_get_info(self.ctx)
+
+    def kernel_times(self) -> dict:
+        return fd_get_kernel_times(self.ctx)
+
+    def reset_kernel_times(self):
+        fd_reset_kernel_times(self.ctx)
 
     def close(self):
         if self.ctx:

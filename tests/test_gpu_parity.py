@@ -290,3 +290,90 @@ def test_torch_allocator_and_stream(fd):
         fdm.fd_reset_allocator()
     for a, b in zip(got, ref[:3]):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# z-slab decomposition on one GPU (FD_OPT_VSLABS): bitwise equal to one slab
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((45, 26, 50), 8), ((96, 300), 4), ((70, 140), 8)])
+@pytest.mark.parametrize("nslabs", [2, 3, 5])
+def test_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs):
+    vel = _rand_vel(dims, seed=21)
+    h, dt = 10.0, 0.5e-3
+    nz = dims[0]
+    z0, z1 = oracle.partition(nz, nslabs, 1)
+    # source on a slab face, a receiver on each side of it and on the last slab
+    src = [((z0,) + tuple(d // 2 for d in dims[1:]), 25.0, 0.02, 1.0),
+           ((z1 - 1,) + tuple(d // 3 for d in dims[1:]), 15.0, 0.03, -0.4)]
+    recs = [(z0 - 1,) + tuple(d // 2 for d in dims[1:]), (z0,) + tuple(d // 2 for d in dims[1:]),
+            (nz - 3,) + tuple(d // 4 for d in dims[1:])]
+    ref = run_gpu(fd, vel, h, dt, order, 33, src, recs)
+    for kernel in (2, 1):
+        got = run_gpu(fd, vel, h, dt, order, 33, src, recs,
+                      options={fd.FD_OPT_VSLABS: nslabs, fd.FD_OPT_KERNEL: kernel})
+        for a, b in zip(got[:3], ref[:3]):
+            assert np.array_equal(a, b), (kernel, nslabs)
+    Po, Ppo, To = oracle.run(vel, h, dt, order, 33, src, recs, nranks=nslabs)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# The paper's unfused decomposition (FD_OPT_KERNEL=3) and per-kernel profiling
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,order", [((30, 40, 70), 2), ((33, 28, 45), 8), ((80, 300), 4)])
+def test_unfused_decomposition_equals_fused(fd, dims, order):
+    vel = _rand_vel(dims, seed=23)
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0)]
+    recs = [tuple(d // 2 + 1 for d in dims), tuple(d // 3 for d in dims)]
+    ref = run_gpu(fd, vel, 10.0, 1e-3, order, 25, src, recs)
+    with fd.Simulation(vel, 10.0, 1e-3, order, options={fd.FD_OPT_KERNEL: 3, fd.FD_OPT_PROFILE: 1}) as sim:
+        for s in src:
+            sim.add_source(*s)
+        sim.set_receivers(recs)
+        sim.step(25)
+        got = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
+        kt = sim.kernel_times()
+        info = sim.info()
+    for a, b in zip(got, ref[:3]):
+        assert np.array_equal(a, b)      # IEEE ==: a band term adds an exact +0
+    assert info["kernel"] == 3
+    names = {"fd_pxx", "fd_pzz", "fd_time", "gather", "inject"} | ({"fd_pyy"} if len(dims) == 3 else set())
+    assert names <= set(kt)
+    assert all(kt[k][1] == 25 for k in ("fd_pxx", "fd_pzz", "fd_time"))
+    assert all(kt[k][0] > 0 for k in kt)
+
+
+def test_profile_counts_fused_launches(fd):
+    dims = (40, 40, 64)
+    vel = _rand_vel(dims, seed=29)
+    with fd.Simulation(vel, 10.0, 1e-3, 4) as sim:
+        sim.add_source((20, 20, 32), 25.0, 0.02)
+        sim.step(3)
+        fd.fd_set_option(sim.ctx, fd.FD_OPT_PROFILE, 1)
+        sim.step(10)
+        kt = sim.kernel_times()
+        assert kt["fused"][1] == 10 and kt["fused"][0] > 0
+        sim.reset_kernel_times()
+        assert sim.kernel_times() == {}
+
+
+@pytest.mark.parametrize("dims,kernel", [((30, 34, 70), 2), ((64, 200), 2), ((30, 34, 70), 1)])
+def test_cuda_graph_replay_bitwise(fd, dims, kernel):
+    """fd_step replays 16-step CUDA graphs (kernels read k from a device
+    counter); results equal plain launches bitwise, across fd_step calls that
+    straddle graph boundaries and trace/wavelet table growth."""
+    vel = _rand_vel(dims, seed=31)
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0), (tuple(d // 3 for d in dims), 12.0, 0.05, -2.0)]
+    recs = [tuple(d // 2 + 1 for d in dims), tuple(d // 4 for d in dims)]
+    outs = []
+    for graph in (0, 1):
+        with fd.Simulation(vel, 10.0, 1e-3, 4, options={fd.FD_OPT_GRAPH: graph, fd.FD_OPT_KERNEL: kernel}) as sim:
+            for s in src:
+                sim.add_source(*s)
+            sim.set_receivers(recs)
+            for n in (5, 40, 17, 33, 1, 64):
+                sim.step(n)
+            outs.append((sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces(),
+                         sim.info()["steps_done"]))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
