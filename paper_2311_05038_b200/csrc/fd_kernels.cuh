@@ -656,6 +656,20 @@ __global__ void gather_receivers_kernel(const StepParams prm) {
     trace_row_of(prm, step_index(prm))[prm.rec.id[j]] = prm.pnext[i];
 }
 
+// K = fl32((v dt / h)^2 / scale) in fp64 (R#7), in place over the uploaded
+// velocities of a pitched buffer; explicit _rn intrinsics, so the result is
+// bitwise the host formula ((double)v * dt / h, squared, / scale, rounded once).
+__global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64_t pitch, double dt, double h,
+                                     double scale) {
+    const int64_t total = rows * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = (t / nx) * pitch + t % nx;
+        const double cv = __ddiv_rn(__dmul_rn((double)buf[i], dt), h);
+        buf[i] = __double2float_rn(__ddiv_rn(__dmul_rn(cv, cv), scale));
+    }
+}
+
 // graph bookkeeping: the device step counter
 __global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
 __global__ void advance_step_kernel(int64_t *kdev, int64_t n) { *kdev += n; }

@@ -346,30 +346,6 @@ static void destroy_all(fd_ctx *c) {
     c->comm_stream = nullptr; c->ev_step = c->ev_comm = nullptr;
 }
 
-// K = (v dt / h)^2 / scale in fp64, rounded once (R#7), into a pitched host
-// array; threads split the planes (host-side setup, off the step path).
-static void compute_K(const fd_ctx *c, const float *v, int64_t nz, std::vector<float> &Kh) {
-    Kh.assign((size_t)(nz * c->nyg * c->pitch), 0.f);
-    const double sc = scale_of(c->R), dt = c->dt, h = c->h;
-    const int64_t nyg = c->nyg, nxg = c->nxg, pitch = c->pitch;
-    auto work = [&](int64_t za, int64_t zb) {
-        for (int64_t z = za; z < zb; ++z)
-            for (int64_t y = 0; y < nyg; ++y) {
-                const float *vr = v + (z * nyg + y) * nxg;
-                float *kr = Kh.data() + (z * nyg + y) * pitch;
-                for (int64_t x = 0; x < nxg; ++x) {
-                    const double cv = (double)vr[x] * dt / h;
-                    kr[x] = (float)(cv * cv / sc);
-                }
-            }
-    };
-    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, nz));
-    nt = std::min(nt, 32);
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) th.emplace_back(work, nz * t / nt, nz * (t + 1) / nt);
-    for (auto &t : th) t.join();
-}
-
 // Allocate a slab's buffers and upload its K: from host velocities v (the
 // slab's planes), or -- when v is NULL -- copied from device K planes kdev.
 static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdev = nullptr) {
@@ -383,9 +359,14 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kde
         return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
     c->dev_bytes += 2.0 * fbytes + kbytes;
     if (v) {
-        std::vector<float> Kh;
-        compute_K(c, v, s.nz, Kh);
-        CUDA_TRY(c, cudaMemcpy(s.K, Kh.data(), kbytes, cudaMemcpyHostToDevice));
+        // upload v into the pitched K buffer, then K = fl32((v dt/h)^2/scale)
+        // in fp64 on the device (bitwise the host formula, R#7)
+        CUDA_TRY(c, cudaMemcpy2D(s.K, c->pitch * 4, v, c->nxg * 4, c->nxg * 4, c->nyg * s.nz,
+                                 cudaMemcpyHostToDevice));
+        const int64_t rows = c->nyg * s.nz;
+        const int blocks = (int)std::min<int64_t>((rows * c->nxg + 255) / 256, 148 * 32);
+        velocity_to_K_kernel<<<blocks, 256>>>(s.K, rows, c->nxg, c->pitch, c->dt, c->h, scale_of(c->R));
+        CUDA_TRY(c, cudaGetLastError());
     } else {
         CUDA_TRY(c, cudaMemcpy(s.K, kdev, kbytes, cudaMemcpyDeviceToDevice));
     }
@@ -517,40 +498,62 @@ static int64_t ntiles_of(const fd_ctx *c, const TileCfg &t) {
 
 // z-chunks for a span of planes: fill one wave of resident CTAs (chunk-major
 // order keeps neighbours in step for L2 halo reuse), chunks >= max(4r, 8) planes.
+// z-chunks for a span of planes.  Measured on B200 (scripts/tune.py,
+// profiles/tune_r01.md): several waves of short-ish units beat one wave of
+// long ones (better balance across the 148 SMs), and within that the wave
+// fill units / (waves * slots) decides.  Aim at ~6 waves (3D) / ~3 waves (2D,
+// whose CTAs are short), then pick among nearby counts the best
+// fill x (chunk / (chunk + warm-up planes)).
 static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
     if (c->opt_zchunks > 0) return (int)std::min<int64_t>(c->opt_zchunks, std::max<int64_t>(1, span));
-    const int64_t slots = (int64_t)c->nsm * occ, ntiles = ntiles_of(c, t);
-    int64_t ch = std::max<int64_t>(1, slots / ntiles);
+    const int64_t slots = (int64_t)c->nsm * std::max(occ, 1), ntiles = ntiles_of(c, t);
     // 3D: chunks of >= max(4r, 8) planes (the 2r warm-up planes stay small);
     // 2D: >= 2 row blocks per chunk
     const int64_t minp = c->ndim == 3 ? std::max(4 * c->R, 8) : 2 * t.ty;
-    ch = std::min<int64_t>(ch, std::max<int64_t>(1, span / minp));
-    return (int)ch;
+    const int64_t chmax = std::max<int64_t>(1, span / minp);
+    const int64_t waves_target = c->ndim == 3 ? 6 : 3;
+    const int64_t target = std::max<int64_t>(1, (waves_target * slots + ntiles / 2) / ntiles);
+    int64_t best = 1;
+    double bscore = -1;
+    for (int64_t ch = std::max<int64_t>(1, target - 3); ch <= target + 3; ++ch) {
+        const int64_t cc = std::min(ch, chmax);
+        const int64_t units = ntiles * cc, waves = (units + slots - 1) / slots;
+        const double fill = (double)units / (double)(waves * slots);
+        const double len = (double)span / (double)cc;
+        const double warm = c->ndim == 3 ? c->R : 0.0;        // ~half the 2r warm-up planes' cost
+        const double score = fill * len / (len + warm);
+        if (score > bscore + 1e-9) { bscore = score; best = cc; }
+    }
+    return (int)best;
 }
 
-// Pick the tile: maximise (wave fill) x (16 B / modelled bytes per point, with
-// the halo re-read and chunk warm-up planes counted).
-static void choose_tile(fd_ctx *c, int64_t span) {
-    const auto &tab = tile_table();
-    double best = -1;
-    int bi = -1, bocc = 0;
-    for (int i = 0; i < (int)tab.size(); ++i) {
-        const TileCfg &t = tab[i];
-        if (t.ndim != c->ndim || t.r != c->R) continue;
-        if (c->opt_tile >= 0 && i != c->opt_tile) continue;
-        const int occ = occupancy(t);
-        if (occ <= 0) continue;
-        const int64_t slots = (int64_t)c->nsm * occ;
-        const int64_t chunks = chunks_for(c, t, occ, span);
-        const int64_t units = ntiles_of(c, t) * chunks;
-        const int64_t waves = (units + slots - 1) / slots;
-        const double fill = (double)units / (double)(waves * slots);
-        const double halo = (double)(t.tx + 8) * (t.ty + 2 * c->R) / ((double)t.tx * t.ty);
-        const double warm = c->ndim == 3 ? (double)(2 * c->R * chunks) / (double)span : 0.0;
-        const double bytes = 12.0 + 4.0 * (halo + warm);
-        const double score = fill * 16.0 / bytes;
-        if (score > best) { best = score; bi = i; bocc = occ; }
+// Preferred tile per (ndim, r), from the r01 sweep: 3D r=1 128x16 (428 Gpts/s
+// on C3), r=2 128x32 (410), r>=3 64x16 with 2 rows/thread (379 at r=4); 2D
+// 64x32 blocks with 3 ring slots (363 / 347 on C2).  Falls back to the first
+// tile that fits when the preferred one does not.
+static bool preferred(const fd_ctx *c, const TileCfg &t) {
+    if (c->ndim == 3) {
+        if (c->R == 1) return t.tx == 128 && t.ty == 16 && t.dp == 2;
+        if (c->R == 2) return t.tx == 128 && t.ty == 32 && t.dp == 2;
+        return t.tx == 64 && t.ty == 16 && t.ny == 2 && t.dp == 2;
     }
+    return t.tx == 64 && t.ty == 32 && t.ny == 4 && t.dp == 3;
+}
+
+static void choose_tile(fd_ctx *c, int64_t span) {
+    (void)span;
+    const auto &tab = tile_table();
+    int bi = -1, bocc = 0;
+    for (int pass = 0; pass < 2 && bi < 0; ++pass)
+        for (int i = 0; i < (int)tab.size(); ++i) {
+            const TileCfg &t = tab[i];
+            if (t.ndim != c->ndim || t.r != c->R) continue;
+            if (c->opt_tile >= 0 ? i != c->opt_tile : (pass == 0 && !preferred(c, t))) continue;
+            const int occ = occupancy(t);
+            if (occ <= 0) continue;
+            bi = i; bocc = occ;
+            break;
+        }
     c->tile = bi;
     c->occ = bocc;
 }

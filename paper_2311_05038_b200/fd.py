@@ -176,8 +176,11 @@ def fd_step(ctx, n: int):
     _check(lib.fd_step(ctx, int(n)), "fd_step")
 
 
-def fd_get_wavefield(ctx, which: int, shape) -> np.ndarray:
-    out = np.empty(tuple(shape), dtype=np.float32)
+def fd_get_wavefield(ctx, which: int, shape, out: np.ndarray | None = None) -> np.ndarray:
+    if out is None:
+        out = np.empty(tuple(shape), dtype=np.float32)
+    elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size != int(np.prod(shape)):
+        raise ValueError("out must be a C-contiguous float32 array of the local field's size")
     _check(lib.fd_get_wavefield(ctx, int(which), out.ctypes.data_as(_f32p)), "fd_get_wavefield")
     return out
 
@@ -286,8 +289,9 @@ class Simulation:
     def step(self, n: int):
         fd_step(self.ctx, n)
 
-    def wavefield(self, which: int = FD_FIELD_CUR) -> np.ndarray:
-        return fd_get_wavefield(self.ctx, which, self.local_shape)
+    def wavefield(self, which: int = FD_FIELD_CUR, out: np.ndarray | None = None) -> np.ndarray:
+        """Copy a field to the host (``out``: optional preallocated, e.g. pinned, buffer)."""
+        return fd_get_wavefield(self.ctx, which, self.local_shape, out)
 
     def set_wavefield(self, which: int, field: np.ndarray):
         fd_set_wavefield(self.ctx, which, field)

@@ -13,7 +13,7 @@ for spec in "C3 2" "C3 8" "C2 2" "C2 8"; do
       --log-file gpurun_out/launches_${TAG}_${cfg}_o${ord}.csv \
       python bench.py --config $cfg --order $ord --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_${cfg}_o${ord}.log 2>&1
   # full capture of one steady-state launch of the fused kernel
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_step -s 5 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5 -c 1 \
       -o gpurun_out/prof_${TAG}_${cfg}_o${ord} -f \
       python bench.py --config $cfg --order $ord --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_${cfg}_o${ord}.log 2>&1
 done

@@ -1,0 +1,41 @@
+#!/usr/bin/env python
+"""Tiny runs of every kernel path for compute-sanitizer:
+
+    compute-sanitizer --tool memcheck  python scripts/sanitize_run.py
+    compute-sanitizer --tool racecheck python scripts/sanitize_run.py
+    compute-sanitizer --tool synccheck python scripts/sanitize_run.py
+    compute-sanitizer --tool initcheck python scripts/sanitize_run.py
+
+Covers the fused 3D and 2D kernels (r = 1 and 4, ragged sizes, several
+z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
+naive and unfused reference paths.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import paper_2311_05038_b200 as fd
+    rng = np.random.default_rng(0)
+    cases = [((19, 21, 37), 2), ((23, 18, 41), 8), ((40, 75), 2), ((45, 70), 8)]
+    for dims, order in cases:
+        vel = rng.uniform(1500, 2500, dims).astype(np.float32)
+        for opts in ({}, {fd.FD_OPT_ZCHUNKS: 3}, {fd.FD_OPT_VSLABS: 2}, {fd.FD_OPT_KERNEL: 1},
+                     {fd.FD_OPT_KERNEL: 3}, {fd.FD_OPT_GRAPH: 0}):
+            with fd.Simulation(vel, 10.0, 5e-4, order, options=opts) as sim:
+                sim.add_source(tuple(d // 2 for d in dims), 25.0, 0.02)
+                sim.set_receivers([tuple(d // 3 for d in dims), tuple(d - 1 for d in dims)])
+                sim.step(20)
+                P = sim.wavefield()
+                T = sim.traces()
+                assert np.all(np.isfinite(P)) and np.all(np.isfinite(T))
+            print("ok", dims, order, opts, flush=True)
+
+
+if __name__ == "__main__":
+    main()
