@@ -169,10 +169,20 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *   FD_OPT_VSLABS    n >= 1: split the grid into n z-slabs on this one GPU with
  *                    device-copy halo exchange (tests the slab logic)
  *   FD_OPT_PROFILE   1: bracket every launch with CUDA events (fd_get_kernel_times)
- * FD_OPT_ASYNC and FD_OPT_PROFILE may change at any time; the others only before
+ *   FD_OPT_TSTEPS    2: temporal blocking -- one launch advances two steps (reads
+ *                    p, p_prev, K once, writes both new fields: 10 B instead of
+ *                    16 B per grid-point update); bitwise equal
+ *                    to single steps.  3D, order <= 4, single-slab contexts.
+ *   FD_OPT_TB2TILE   index of the temporal-blocking tile configuration (-1 auto)
+ *   FD_OPT_RESERVE   n >= 0: finish setup now -- allocate the step tables for n more
+ *                    steps and capture the CUDA graphs the next fd_step calls will
+ *                    replay -- so no allocation, synchronisation or capture happens
+ *                    inside a later timed fd_step (marks the context started)
+ * FD_OPT_ASYNC, FD_OPT_PROFILE and FD_OPT_RESERVE may be set at any time; the others only before
  * the first fd_step.  Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
 enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
-       FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7 };
+       FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7, FD_OPT_TSTEPS = 8,
+       FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10 };
 fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
 
 /* Device time per kernel kind accumulated while FD_OPT_PROFILE = 1 (ms and launch

@@ -62,7 +62,8 @@ struct StepParams {
     int32_t zlo, zhi;       // local planes computed by this launch
     int32_t ntx, nty;       // tiles along x, y
     int32_t nchunks;        // z-chunks of [zlo, zhi)
-    float *pnext;           // base of the p_prev buffer (overwritten in place)
+    float *pnext;           // base of the p_prev buffer (overwritten in place); TB2: the C buffer
+    float *pnext2;          // TB2 only: the D buffer (P^{k+2})
     const float *p;         // base of the p buffer (naive kernel only)
     const float *K;         // K base (naive kernel only)
     // step index: k, or *kdev + koff when replayed from a CUDA graph

@@ -18,6 +18,7 @@
 
 #include "../../include/fd.h"
 #include "fd_kernels.cuh"
+#include "fd_tb2.cuh"
 
 using namespace fdk;
 
@@ -156,6 +157,28 @@ static const std::vector<TileCfg> &tile_table() {
 }
 
 // ------------------------------------------------------------------ context
+// Two-steps-per-pass (temporal blocking) tiles, 3D, r <= 2 (fd_tb2.cuh).
+// Presented as TileCfg so the chunking/receiver code is shared: pbw/pbz hold
+// the P^k box (BX0, BY0), tbw/tbz the grown-tile box (BXE, BYE).
+template <class C>
+static void launch_tb2(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
+                       const CUtensorMap &c, const StepParams &p) {
+    tb2_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
+}
+template <int R, int TX, int TY, int NYA, int NYB, int DP, int DA, int NC>
+static TileCfg make_tb2() {
+    using C = CfgTB<R, TX, TY, NYA, NYB, DP, DA, NC>;
+    return TileCfg{3, R, TX, TY, NYB, DP, DA, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES,
+                   (const void *)tb2_step_kernel<C>, launch_tb2<C>};
+}
+static const std::vector<TileCfg> &tb2_table() {
+    static const std::vector<TileCfg> t = {
+        make_tb2<1, 64, 16, 2, 1, 2, 2, 256>(), make_tb2<1, 64, 16, 3, 2, 2, 2, 128>(),
+        make_tb2<1, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<1, 128, 16, 3, 2, 1, 1, 256>(),
+        make_tb2<2, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<2, 64, 16, 4, 2, 1, 1, 128>()};
+    return t;
+}
+
 // ------------------------------------------------------------------ NCCL (dlopen)
 // NCCL is loaded at run time (libnccl.so.2: torch's bundled copy when torch has
 // loaded it, else the system one) so the library loads on machines without it.
@@ -224,11 +247,14 @@ struct Region {
 // each side).  One per context, except FD_OPT_VSLABS (several on one GPU).
 struct Slab {
     int64_t z0 = 0, z1 = 0, nz = 0;
-    float *A = nullptr, *B = nullptr, *K = nullptr;
+    float *F[4] = {nullptr, nullptr, nullptr, nullptr};   // field buffers (F[2], F[3]: TB2 only)
+    float *K = nullptr;
     float *D[3] = {nullptr, nullptr, nullptr};   // Pxx, Pyy, Pzz (unfused decomposition only)
     float *d_src_raw = nullptr;
-    CUtensorMap mA_halo, mB_halo, mA_tile, mB_tile, mK;
+    CUtensorMap mHalo[4], mTile[4], mK;        // single-step kernel maps per field buffer
+    CUtensorMap mP0[4], mPm[4], mKe;           // TB2 maps
     std::vector<Region> regions;
+    Region tb2;                                 // the TB2 launch (own tiles -> own receiver CSR)
 };
 
 struct fd_ctx {
@@ -246,7 +272,7 @@ struct fd_ctx {
     cudaStream_t stream = nullptr;        // user stream (interior kernels)
     cudaStream_t comm_stream = nullptr;   // boundary kernels + NCCL (distributed)
     cudaEvent_t ev_step = nullptr, ev_comm = nullptr;
-    bool cur_is_A = true;
+    int icur = 0, iprev = 1;              // roles of the slabs' field buffers
     std::vector<SourceDef> src;
     std::vector<RecDef> rec;
     std::vector<Slab> slabs;
@@ -258,9 +284,8 @@ struct fd_ctx {
     cudaStream_t own_stream = nullptr;    // used when no stream was set (capturable)
     // CUDA graphs of G steps (one per starting buffer parity), re-captured when
     // the trace / wavelet tables move
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    const void *gkey[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    int64_t glaunches = 0;
+    struct Graph { int icur, iprev, end_icur, end_iprev; cudaGraphExec_t exec; const void *kt, *kw; int64_t launches; };
+    std::vector<Graph> graphs;
     bool capturing = false;
     int64_t gk0 = 0;
     // distributed
@@ -270,6 +295,9 @@ struct fd_ctx {
     // kernel configuration
     int opt_kernel = 0, opt_tile = -1, opt_zchunks = 0, opt_async = 0, opt_graph = 1, opt_vslabs = 1;
     int opt_profile = 0;
+    int opt_tsteps = 1;                   // 2: temporal blocking (two steps per launch)
+    int opt_tb2tile = -1;
+    int tb2 = -1, tb2occ = 0;             // chosen tb2_table() entry
     bool overlap = false;                 // boundary/interior split on two streams
     int tile = -1, occ = 0, nsm = 148;
     // FD_OPT_PROFILE: CUDA events around every launch, folded into per-kernel sums
@@ -283,8 +311,8 @@ struct fd_ctx {
 
 static inline int64_t plane_floats(const fd_ctx *c) { return c->nyg * c->pitch; }
 static inline int64_t buf_floats(const fd_ctx *c, const Slab &s) { return (s.nz + 2 * c->R) * plane_floats(c); }
-static inline float *cur_buf(const fd_ctx *c, const Slab &s) { return c->cur_is_A ? s.A : s.B; }
-static inline float *prev_buf(const fd_ctx *c, const Slab &s) { return c->cur_is_A ? s.B : s.A; }
+static inline float *cur_buf(const fd_ctx *c, const Slab &s) { return s.F[c->icur]; }
+static inline float *prev_buf(const fd_ctx *c, const Slab &s) { return s.F[c->iprev]; }
 
 static double scale_of(int R) { return tap_scale(R); }
 
@@ -316,14 +344,18 @@ static fd_status partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_
 
 static void free_slab(Slab &s) {
     for (auto &d : s.D) { dev_free(d); d = nullptr; }
-    dev_free(s.A); dev_free(s.B); dev_free(s.K); dev_free(s.d_src_raw);
-    s.A = s.B = s.K = s.d_src_raw = nullptr;
+    for (auto &f : s.F) { dev_free(f); f = nullptr; }
+    dev_free(s.K); dev_free(s.d_src_raw);
+    s.K = s.d_src_raw = nullptr;
     for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
+    dev_free(s.tb2.d_rec);
+    s.tb2.d_rec = nullptr;
 }
 
 static void drop_graphs(fd_ctx *c) {
-    for (auto &g : c->gexec)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (auto &g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
 }
 
 static void destroy_all(fd_ctx *c) {
@@ -351,11 +383,11 @@ static void destroy_all(fd_ctx *c) {
 static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdev = nullptr) {
     const size_t fbytes = (size_t)buf_floats(c, s) * 4;
     const size_t kbytes = (size_t)(s.nz * plane_floats(c)) * 4;
-    s.A = (float *)dev_alloc(fbytes);
-    s.B = (float *)dev_alloc(fbytes);
+    s.F[0] = (float *)dev_alloc(fbytes);
+    s.F[1] = (float *)dev_alloc(fbytes);
     s.K = (float *)dev_alloc(kbytes);
     s.d_src_raw = (float *)dev_alloc(kMaxSources * 4);
-    if (!s.A || !s.B || !s.K || !s.d_src_raw)
+    if (!s.F[0] || !s.F[1] || !s.K || !s.d_src_raw)
         return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
     c->dev_bytes += 2.0 * fbytes + kbytes;
     if (v) {
@@ -370,8 +402,8 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kde
     } else {
         CUDA_TRY(c, cudaMemcpy(s.K, kdev, kbytes, cudaMemcpyDeviceToDevice));
     }
-    CUDA_TRY(c, cudaMemset(s.A, 0, fbytes));
-    CUDA_TRY(c, cudaMemset(s.B, 0, fbytes));
+    CUDA_TRY(c, cudaMemset(s.F[0], 0, fbytes));
+    CUDA_TRY(c, cudaMemset(s.F[1], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.d_src_raw, 0, kMaxSources * 4));
     return FD_OK;
 }
@@ -564,11 +596,12 @@ static fd_status make_maps(fd_ctx *c, Slab &s) {
     // 3D: boxes (x, y) of one plane; 2D: boxes of pbz / tbz rows (nyg = 1)
     const int hy = c->ndim == 3 ? c->R : 0;
     const int pby = c->ndim == 3 ? t.ty + 2 * hy : 1, tby = c->ndim == 3 ? t.ty : 1;
-    bool ok = make_map(&s.mA_halo, s.A, c->nxg, c->nyg, planes, c->pitch, t.pbw, pby, t.pbz) &&
-              make_map(&s.mB_halo, s.B, c->nxg, c->nyg, planes, c->pitch, t.pbw, pby, t.pbz) &&
-              make_map(&s.mA_tile, s.A, c->nxg, c->nyg, planes, c->pitch, t.tbw, tby, t.tbz) &&
-              make_map(&s.mB_tile, s.B, c->nxg, c->nyg, planes, c->pitch, t.tbw, tby, t.tbz) &&
-              make_map(&s.mK, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, tby, t.tbz);
+    bool ok = make_map(&s.mK, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, tby, t.tbz);
+    for (int b = 0; b < 4 && ok; ++b) {
+        if (!s.F[b]) continue;
+        ok = make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, pby, t.pbz) &&
+             make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, tby, t.tbz);
+    }
     if (!ok) {
         c->poisoned = true;
         return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -578,12 +611,11 @@ static fd_status make_maps(fd_ctx *c, Slab &s) {
 
 // Receivers of a region, sorted by (work unit, z) with CSR offsets per unit
 // (fused kernel) -- or a flat list (naive kernel).
-static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g) {
+static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g, const TileCfg *t) {
     dev_free(g.d_rec);
     g.d_rec = nullptr;
     struct L { int32_t unit, z, y, x, id; };
     std::vector<L> loc;
-    const TileCfg *t = (c->opt_kernel != 0) ? nullptr : &tile_table()[c->tile];
     int ntx = 1, ntiles = 1;
     if (t) {
         ntx = (int)((c->nxg + t->tx - 1) / t->tx);
@@ -650,8 +682,8 @@ static fd_status split_virtual(fd_ctx *c, int n) {
         st = build_slab(c, s, nullptr, o.K + a * pf);
         if (st) break;
         const size_t bytes = (size_t)(s.nz * pf) * 4;
-        CUDA_TRY(c, cudaMemcpy(s.A + c->R * pf, o.A + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
-        CUDA_TRY(c, cudaMemcpy(s.B + c->R * pf, o.B + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
+        for (int f = 0; f < 2; ++f)
+            CUDA_TRY(c, cudaMemcpy(s.F[f] + c->R * pf, o.F[f] + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
     }
     free_slab(o);
     c->slabs.swap(ns);
@@ -719,9 +751,48 @@ static fd_status prepare(fd_ctx *c) {
             add(0, nz, false);
         }
         for (auto &g : s.regions) {
-            st = upload_region_receivers(c, s, g);
+            st = upload_region_receivers(c, s, g, c->opt_kernel != 0 ? nullptr : &tile_table()[c->tile]);
             if (st) return st;
         }
+    }
+    if (c->opt_tsteps == 2) {
+        // temporal blocking: 3D, r <= 2, one slab, fused path
+        if (c->ndim != 3 || c->R > 2 || c->slabs.size() != 1 || c->nranks != 1 || c->opt_kernel != 0)
+            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs a 3D single-slab context with r <= 2 and the fused kernel");
+        const auto &tb = tb2_table();
+        for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
+            if (tb[i].r != c->R || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
+            const int occ = occupancy(tb[i]);
+            if (occ > 0) { c->tb2 = i; c->tb2occ = occ; }
+        }
+        if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
+        const TileCfg &t = tb[c->tb2];
+        CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
+        Slab &s = c->slabs[0];
+        const size_t fbytes = (size_t)buf_floats(c, s) * 4;
+        for (int b = 2; b < 4; ++b) {
+            s.F[b] = (float *)dev_alloc(fbytes);
+            if (!s.F[b]) return fail(FD_ERR_NOMEM, "temporal-blocking buffer allocation failed");
+            CUDA_TRY(c, cudaMemset(s.F[b], 0, fbytes));
+            c->dev_bytes += (double)fbytes;
+        }
+        const TileCfg &ts = tile_table()[c->tile];
+        const int64_t planes = s.nz + 2 * c->R;
+        bool ok = make_map(&s.mKe, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, t.tbz, 1);
+        for (int b = 0; b < 4 && ok; ++b)
+            ok = make_map(&s.mP0[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, t.pbz, 1) &&
+                 make_map(&s.mPm[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, t.tbz, 1) &&
+                 make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.pbw, ts.ty + 2 * c->R, 1) &&
+                 make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.tbw, ts.ty, 1);
+        if (!ok) {
+            c->poisoned = true;
+            return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed (temporal blocking)");
+        }
+        s.tb2.zlo = 0;
+        s.tb2.zhi = (int32_t)s.nz;
+        s.tb2.zchunks = chunks_for(c, t, c->tb2occ, s.nz);
+        st = upload_region_receivers(c, s, s.tb2, &t);
+        if (st) return st;
     }
     if (overlap) {
         int lo = 0, hi = 0;
@@ -929,8 +1000,8 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
     const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
-    const CUtensorMap &mp = c->cur_is_A ? s.mA_halo : s.mB_halo;
-    const CUtensorMap &mpp = c->cur_is_A ? s.mB_tile : s.mA_tile;
+    const CUtensorMap &mp = s.mHalo[c->icur];
+    const CUtensorMap &mpp = s.mTile[c->iprev];
     tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
@@ -1007,8 +1078,47 @@ static fd_status one_step(fd_ctx *c) {
         }
     }
     CUDA_TRY(c, cudaGetLastError());
-    c->cur_is_A = !c->cur_is_A;
+    std::swap(c->icur, c->iprev);
     ++c->k;
+    return FD_OK;
+}
+
+// One temporal-blocking launch: steps k and k+1 (fd_tb2.cuh).  Reads the
+// (cur, prev) buffers, writes P^{k+1} and P^{k+2} into the two free ones.
+static fd_status two_steps(fd_ctx *c) {
+    Slab &s = c->slabs[0];
+    Region &g = s.tb2;
+    const TileCfg &t = tb2_table()[c->tb2];
+    int f1 = -1, f2 = -1;
+    for (int b = 0; b < 4; ++b)
+        if (b != c->icur && b != c->iprev) (f1 < 0 ? f1 : f2) = b;
+    StepParams p;
+    fill_params(c, s, &g, p, c->k);
+    p.p = cur_buf(c, s);
+    p.pnext = s.F[f1];
+    p.pnext2 = s.F[f2];
+    p.K = s.K;
+    p.ntx = (int32_t)((c->nxg + t.tx - 1) / t.tx);
+    p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
+    const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
+    g.ctas = (int)grid.x;
+    const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
+    tracked(c, FD_K_FUSED, c->stream, [&] { t.launch(grid, t.smem, c->stream, m0, mm, s.mKe, p); });
+    CUDA_TRY(c, cudaGetLastError());
+    c->iprev = f1;
+    c->icur = f2;
+    c->k += 2;
+    return FD_OK;
+}
+
+// Advance m steps with plain launches (pairs through temporal blocking).
+static fd_status advance_plain(fd_ctx *c, int64_t m) {
+    const bool tb = c->opt_tsteps == 2 && c->tb2 >= 0;
+    while (m > 0) {
+        fd_status s = (tb && m >= 2) ? two_steps(c) : one_step(c);
+        if (s) return s;
+        m -= (tb && m >= 2) ? 2 : 1;
+    }
     return FD_OK;
 }
 
@@ -1023,36 +1133,73 @@ static bool graphs_usable(const fd_ctx *c) {
     return c->opt_graph && !c->overlap && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream;
 }
 
-static fd_status capture_graph(fd_ctx *c, int par) {
+// Capture kGraphSteps steps starting from the current buffer roles; the
+// entry records the roles it ends in.  Returns the entry index or -1.
+static int capture_graph(fd_ctx *c, fd_status *st) {
     const int64_t k0 = c->k, l0 = c->launches;
-    const bool a0 = c->cur_is_A;
+    const int ic0 = c->icur, ip0 = c->iprev;
+    *st = FD_OK;
     cudaGraph_t graph = nullptr;
-    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { cudaGetLastError(); c->opt_graph = 0; return -1; }
     c->capturing = true;
     c->gk0 = k0;
-    fd_status s = FD_OK;
-    for (int64_t i = 0; i < kGraphSteps && s == FD_OK; ++i) s = one_step(c);
+    fd_status s = advance_plain(c, kGraphSteps);
     advance_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, kGraphSteps);
     c->capturing = false;
-    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-    c->glaunches = c->launches - l0 + 1;
-    c->k = k0; c->cur_is_A = a0; c->launches = l0;
-    if (s) { if (graph) cudaGraphDestroy(graph); return s; }
+    e = cudaStreamEndCapture(c->stream, &graph);
+    fd_ctx::Graph gr{ic0, ip0, c->icur, c->iprev, nullptr, c->d_traces, c->d_wtab, c->launches - l0 + 1};
+    c->k = k0; c->icur = ic0; c->iprev = ip0; c->launches = l0;
+    if (s) { if (graph) cudaGraphDestroy(graph); *st = s; return -1; }
     if (e != cudaSuccess || !graph) {
         cudaGetLastError();
         c->opt_graph = 0;                 // fall back to plain launches
-        return FD_OK;
+        return -1;
     }
-    e = cudaGraphInstantiate(&c->gexec[par], graph, 0);
+    e = cudaGraphInstantiate(&gr.exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        c->gexec[par] = nullptr;
         c->opt_graph = 0;
-        return FD_OK;
+        return -1;
     }
-    c->gkey[par][0] = c->d_traces;
-    c->gkey[par][1] = c->d_wtab;
+    c->graphs.push_back(gr);
+    return (int)c->graphs.size() - 1;
+}
+
+// FD_OPT_RESERVE: prepare the context, grow the step tables for n more steps
+// and capture the graphs the next fd_step calls will replay, so that none of
+// that setup (allocation, synchronisation, capture) lands inside a timed region.
+static fd_status reserve_steps(fd_ctx *c, int64_t n) {
+    fd_status s;
+    if (!c->started) {
+        s = prepare(c);
+        if (s) return s;
+        c->started = true;
+    }
+    s = ensure_tables(c, c->k + n);
+    if (s) return s;
+    if (graphs_usable(c) && n >= kGraphSteps) {
+        int ic = c->icur, ip = c->iprev;
+        for (int guard = 0; guard < 8; ++guard) {
+            const int sic = c->icur, sip = c->iprev;
+            c->icur = ic; c->iprev = ip;
+            int gi = -1;
+            for (size_t q = 0; q < c->graphs.size(); ++q)
+                if (c->graphs[q].icur == ic && c->graphs[q].iprev == ip && c->graphs[q].kt == c->d_traces &&
+                    c->graphs[q].kw == c->d_wtab)
+                    gi = (int)q;
+            if (gi < 0) gi = capture_graph(c, &s);
+            c->icur = sic; c->iprev = sip;
+            if (s) return s;
+            if (gi < 0) break;
+            const int nic = c->graphs[gi].end_icur, nip = c->graphs[gi].end_iprev;
+            if (nic == c->icur && nip == c->iprev) break;
+            if (nic == ic && nip == ip) break;
+            ic = nic; ip = nip;
+        }
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return FD_OK;
 }
 
@@ -1164,25 +1311,33 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         set_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, c->k);
         ++c->launches;
         for (; n - i >= kGraphSteps; i += kGraphSteps) {
-            const int par = c->cur_is_A ? 0 : 1;
-            if (c->gexec[par] && (c->gkey[par][0] != c->d_traces || c->gkey[par][1] != c->d_wtab)) {
-                cudaGraphExecDestroy(c->gexec[par]);
-                c->gexec[par] = nullptr;
+            int gi = -1;
+            for (size_t q = 0; q < c->graphs.size(); ++q) {
+                auto &g = c->graphs[q];
+                if (g.icur != c->icur || g.iprev != c->iprev) continue;
+                if (g.kt != c->d_traces || g.kw != c->d_wtab) {   // tables moved: re-capture
+                    cudaGraphExecDestroy(g.exec);
+                    c->graphs.erase(c->graphs.begin() + q);
+                    break;
+                }
+                gi = (int)q;
+                break;
             }
-            if (!c->gexec[par]) {
-                s = capture_graph(c, par);
+            if (gi < 0) {
+                gi = capture_graph(c, &s);
                 if (s) return s;
-                if (!c->gexec[par]) break;   // capture unsupported: plain launches
+                if (gi < 0) break;               // capture unsupported: plain launches
             }
-            CUDA_TRY(c, cudaGraphLaunch(c->gexec[par], c->stream));
-            c->k += kGraphSteps;             // G even: buffer parity unchanged
-            c->launches += c->glaunches;
+            auto &g = c->graphs[gi];
+            CUDA_TRY(c, cudaGraphLaunch(g.exec, c->stream));
+            c->k += kGraphSteps;
+            c->icur = g.end_icur;
+            c->iprev = g.end_iprev;
+            c->launches += g.launches;
         }
     }
-    for (; i < n; ++i) {
-        s = one_step(c);
-        if (s) return s;
-    }
+    s = advance_plain(c, n - i);
+    if (s) return s;
     if (!c->opt_async) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (c->comm && nccl().CommGetAsyncError) {
         ncclResult_t ae = 0;
@@ -1307,6 +1462,10 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
     fd_status s = check_ctx(c);
     if (s) return s;
     if (key == FD_OPT_ASYNC) { c->opt_async = v ? 1 : 0; return FD_OK; }
+    if (key == FD_OPT_RESERVE) {
+        if (v < 0) return fail(FD_ERR_ARG, "FD_OPT_RESERVE must be >= 0");
+        return reserve_steps(c, v);
+    }
     if (key == FD_OPT_PROFILE) {
         s = fold_times(c);
         if (s) return s;
@@ -1330,6 +1489,16 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
     case FD_OPT_ZCHUNKS:
         if (v < 0 || v > 4096) return fail(FD_ERR_ARG, "bad zchunks");
         c->opt_zchunks = (int)v;
+        return FD_OK;
+    case FD_OPT_TSTEPS:
+        if (v != 1 && v != 2) return fail(FD_ERR_ARG, "FD_OPT_TSTEPS must be 1 or 2");
+        if (v == 2 && (c->ndim != 3 || c->R > 2))
+            return fail(FD_ERR_ARG, "FD_OPT_TSTEPS=2 is implemented for 3D grids with order <= 4");
+        c->opt_tsteps = (int)v;
+        return FD_OK;
+    case FD_OPT_TB2TILE:
+        if (v < -1 || v >= (int64_t)tb2_table().size()) return fail(FD_ERR_ARG, "tb2 tile index out of range");
+        c->opt_tb2tile = (int)v;
         return FD_OK;
     case FD_OPT_GRAPH: c->opt_graph = v ? 1 : 0; return FD_OK;
     case FD_OPT_VSLABS:
@@ -1376,6 +1545,16 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->device_bytes = c->dev_bytes;
     if (c->opt_kernel != 0) { o->kernel = c->opt_kernel; return FD_OK; }
     o->kernel = 2;
+    if (c->opt_tsteps == 2 && c->tb2 >= 0) {
+        const TileCfg &t = tb2_table()[c->tb2];
+        const Region &g = c->slabs[0].tb2;
+        o->tile_x = t.tx; o->tile_y = t.ty; o->rows_per_thread = t.ny;
+        o->p_stages = 2 * t.r + 1 + t.dp; o->k_stages = t.r + 1 + t.dk;
+        o->threads_per_cta = t.threads; o->smem_bytes = t.smem;
+        o->zchunks = g.zchunks;
+        o->ctas = (int)(ntiles_of(c, t) * g.zchunks);
+        return FD_OK;
+    }
     if (!c->started) choose_tile(c, c->z1 - c->z0);
     if (c->tile >= 0) {
         const TileCfg &t = tile_table()[c->tile];

@@ -22,6 +22,7 @@ FD_FIELD_CUR, FD_FIELD_PREV = 0, 1
 FD_FLAG_ALLOW_UNSTABLE = 1
 FD_OPT_KERNEL, FD_OPT_TILE, FD_OPT_ZCHUNKS, FD_OPT_ASYNC, FD_OPT_GRAPH, FD_OPT_VSLABS = 1, 2, 3, 4, 5, 6
 FD_OPT_PROFILE = 7
+FD_OPT_TSTEPS, FD_OPT_TB2TILE, FD_OPT_RESERVE = 8, 9, 10
 KERNEL_KINDS = ["fused", "naive", "gather", "inject", "fd_pxx", "fd_pyy", "fd_pzz", "fd_time", "halo"]
 
 EXPORTED = [
@@ -288,6 +289,10 @@ class Simulation:
 
     def step(self, n: int):
         fd_step(self.ctx, n)
+
+    def reserve(self, n: int):
+        """Finish setup for n more steps (tables, CUDA graphs) outside any timed region."""
+        fd_set_option(self.ctx, FD_OPT_RESERVE, n)
 
     def wavefield(self, which: int = FD_FIELD_CUR, out: np.ndarray | None = None) -> np.ndarray:
         """Copy a field to the host (``out``: optional preallocated, e.g. pinned, buffer)."""

@@ -69,10 +69,10 @@ def main(tag):
              "launch of the fused step kernel; launch lists with gpu__time_duration.sum).  Algorithmic bytes",
              "= 16 B x grid points per launch (DESIGN.md section 5.4).", ""]
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
-        m = re.match(rf"prof_{tag}_(C\d)_o(\d)\.ncu-rep", os.path.basename(rep))
+        m = re.match(rf"prof_{tag}_(C\d)_o(\d)(_tb2)?\.ncu-rep", os.path.basename(rep))
         if not m:
             continue
-        wl, order = m.group(1), int(m.group(2))
+        wl, order, tb2 = m.group(1), int(m.group(2)), bool(m.group(3))
         d = raw(rep)
         rd = to_bytes(*d["dram__bytes_read.sum"])
         wr = to_bytes(*d["dram__bytes_write.sum"])
@@ -80,13 +80,13 @@ def main(tag):
         dur = float(d["gpu__time_duration.sum"][0].replace(",", ""))
         dunit = d["gpu__time_duration.sum"][1]
         dur_s = dur * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-9)
-        alg = 16.0 * npts
-        summ[f"{wl}:o{order}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+        alg = (20.0 if tb2 else 16.0) * npts
+        summ[f"{wl}:o{order}{':tb2' if tb2 else ''}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                   "algorithmic_bytes": alg, "bytes_per_point": (rd + wr) / npts,
                                   "ncu_duration_s": dur_s, "tag": tag}
-        lines += [f"## {wl}, order {order}", "",
+        lines += [f"## {wl}, order {order}{' (temporal blocking, 2 steps per launch)' if tb2 else ''}", "",
                   f"* DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB = {(rd + wr) / npts:.2f} B/pt "
-                  f"(algorithmic 16 B/pt = {alg / 1e9:.3f} GB)",
+                  f"(algorithmic {alg / npts:.0f} B/pt = {alg / 1e9:.3f} GB)",
                   f"* ncu duration {dur_s * 1e6:.1f} us -> {(rd + wr) / dur_s / 1e9:.0f} GB/s DRAM, "
                   f"{alg / dur_s / 1e9:.0f} GB/s algorithmic", "", "| metric | value |", "|---|---|"]
         for key, name in METRICS:

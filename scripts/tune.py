@@ -20,6 +20,7 @@ def main():
     ap.add_argument("specs", nargs="+")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--zchunks", default="0")
+    ap.add_argument("--tsteps", type=int, default=1)
     args = ap.parse_args()
     import torch
     import paper_2311_05038_b200 as fd
@@ -34,8 +35,12 @@ def main():
         for tile in range(64):
             for zc in [int(z) for z in args.zchunks.split(",")]:
                 try:
-                    sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream.cuda_stream,
-                                        options={fd.FD_OPT_TILE: tile, fd.FD_OPT_ZCHUNKS: zc, fd.FD_OPT_ASYNC: 1})
+                    opts = {fd.FD_OPT_ZCHUNKS: zc, fd.FD_OPT_ASYNC: 1}
+                    if args.tsteps == 2:
+                        opts.update({fd.FD_OPT_TSTEPS: 2, fdm.FD_OPT_TB2TILE: tile})
+                    else:
+                        opts[fd.FD_OPT_TILE] = tile
+                    sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream.cuda_stream, options=opts)
                 except fdm.FDError as e:
                     if "tile" in e.detail:
                         continue
@@ -43,7 +48,14 @@ def main():
                 for s in wl.sources:
                     sim.add_source(s.idx, s.f, s.t0, s.amp)
                 sim.set_receivers(wl.receivers)
-                sim.step(5)
+                try:
+                    sim.step(6)
+                except fdm.FDError as e:
+                    sim.close()
+                    if e.status in (-5, -7) and "temporal" in e.detail:   # tb2 tile for another order
+                        continue
+                    raise
+                sim.reserve(args.steps)
                 stream.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -54,7 +66,7 @@ def main():
                 info = sim.info()
                 sim.close()
                 g = wl.npts / (ms / 1e3) / 1e9
-                rec = {"workload": name, "order": wl.order, "tile": tile, "tx": info["tile_x"],
+                rec = {"workload": name, "order": wl.order, "tile": tile, "tsteps": args.tsteps, "tx": info["tile_x"],
                        "ty": info["tile_y"], "ny": info["rows_per_thread"], "zchunks": info["zchunks"],
                        "ctas": info["ctas"], "threads": info["threads_per_cta"], "smem": info["smem_bytes"],
                        "ms": ms, "gpts": g, "frac_16B_6549": g * 16 / 6549.4}

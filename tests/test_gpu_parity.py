@@ -377,3 +377,71 @@ def test_cuda_graph_replay_bitwise(fd, dims, kernel):
                          sim.info()["steps_done"]))
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# Temporal blocking (FD_OPT_TSTEPS=2): two steps per launch, bitwise = single
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,order", [((37, 45, 70), 2), ((30, 33, 131), 2), ((41, 29, 66), 4),
+                                        ((24, 70, 140), 4)])
+def test_temporal_blocking_bitwise(fd, oracle, dims, order):
+    from paper_2311_05038_b200 import fd as fdm
+    vel = _rand_vel(dims, seed=37)
+    h, dt = 10.0, 0.5e-3
+    # sources on tile / chunk boundaries and one shared point; receivers near them
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0),
+           ((dims[0] // 3, 16, 64 if dims[2] > 70 else 63), 18.0, 0.03, -0.6),
+           (tuple(d // 2 for d in dims), 12.0, 0.04, 0.3)]
+    recs = [tuple(d // 2 for d in dims), (dims[0] // 3, 15, 63), (dims[0] - 3, 17, 5), (1, 1, 1)]
+    ref = run_gpu(fd, vel, h, dt, order, 41, src, recs)
+    ntb = 0
+    for tile in range(8):
+        for zc in (0, 1, 3):
+            for graph in (1, 0):
+                try:
+                    got = run_gpu(fd, vel, h, dt, order, 41, src, recs,
+                                  options={fd.FD_OPT_TSTEPS: 2, fdm.FD_OPT_TB2TILE: tile,
+                                           fd.FD_OPT_ZCHUNKS: zc, fd.FD_OPT_GRAPH: graph})
+                except fdm.FDError as e:
+                    assert e.status in (-1, -5, -7), e
+                    break
+                ntb += 1
+                for a, b in zip(got[:3], ref[:3]):
+                    assert np.array_equal(a, b), (tile, zc, graph)
+    assert ntb >= 2
+    Po, _, To = oracle.run(vel, h, dt, order, 41, src, recs)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+def test_temporal_blocking_incremental_odd_steps(fd):
+    dims = (40, 36, 96)
+    vel = _rand_vel(dims, seed=41)
+    src = [((20, 18, 48), 25.0, 0.02, 1.0)]
+    recs = [(20, 18, 50), (25, 10, 90)]
+    ref = run_gpu(fd, vel, 10.0, 1e-3, 2, 91, src, recs)
+    with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_TSTEPS: 2}) as sim:
+        sim.add_source(*src[0])
+        sim.set_receivers(recs)
+        for n in (1, 2, 33, 0, 17, 38):
+            sim.step(n)
+        got = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
+    for a, b in zip(got, ref[:3]):
+        assert np.array_equal(a, b)
+
+
+def test_reserve_then_step_bitwise(fd):
+    dims = (30, 40, 70)
+    vel = _rand_vel(dims, seed=43)
+    src = [((15, 20, 35), 25.0, 0.02, 1.0)]
+    recs = [(15, 20, 40)]
+    ref = run_gpu(fd, vel, 10.0, 1e-3, 2, 70, src, recs)
+    for ts in (1, 2):
+        with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_TSTEPS: ts}) as sim:
+            sim.add_source(*src[0])
+            sim.set_receivers(recs)
+            sim.step(3)
+            sim.reserve(200)
+            sim.step(67)
+            got = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
+        for a, b in zip(got, ref[:3]):
+            assert np.array_equal(a, b), ts
