@@ -186,39 +186,50 @@ def cpu_oracle_sample(wl, budget_s: float = 15.0):
 
 
 def run_reference(args, wl):
+    """The tier's reference arm: the fp64 oracle, as it stands, on the host
+    cores.  W warm-up steps, then exactly K timed steps in one oracle call on
+    a bounded slab of the workload (full-width planes around the source plane),
+    the slab sized from a calibration step so the K steps take ~--ref-budget s."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     import oracle
+    from workloads import velocity
     oracle.build()
     cores = oracle.max_threads()
-    # bounded per-step sample: nz_s full-width planes, sized for ~0.15 s per step
-    vel_full_dims = wl.dims
-    plane = int(np.prod(vel_full_dims[1:]))
-    nz_s = max(2 * (wl.order // 2) + 1, min(wl.dims[0], int(3.0e7 / plane) or 1))
-    dims_s = (nz_s,) + tuple(vel_full_dims[1:])
-    from workloads import velocity
-    vel = velocity(wl.model, dims_s, nz_global=wl.dims[0])
-    srcz = nz_s // 2
-    src = [((srcz,) + tuple(s.idx[1:]), s.f, s.t0, s.amp) for s in wl.sources]
-    P = np.zeros(dims_s)
-    Pm = np.zeros(dims_s)
-    for _ in range(args.warmup):
-        P, Pm, _ = oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, P0=P, Pm1=Pm, nthreads=cores)
+    plane = int(np.prod(wl.dims[1:]))
+
+    def sample(nz_s):
+        dims_s = (nz_s,) + tuple(wl.dims[1:])
+        vel = velocity(wl.model, dims_s, nz_global=wl.dims[0])
+        src = [((nz_s // 2,) + tuple(s.idx[1:]), s.f, s.t0, s.amp) for s in wl.sources]
+        return dims_s, vel, src
+
+    # calibration: one step on a small slab
+    dims_c, vel_c, src_c = sample(max(2 * (wl.order // 2) + 1, min(wl.dims[0], 32)))
+    rate = 0.0
+    for _ in range(2):                         # the first call also loads the library
+        t0 = time.perf_counter()
+        oracle.run(vel_c, wl.h, wl.dt, wl.order, 4, src_c, nthreads=cores)
+        rate = max(rate, 4 * int(np.prod(dims_c)) / (time.perf_counter() - t0))   # points/s
+    nz_s = int(rate * args.ref_budget / max(args.steps, 1) / plane)
+    nz_s = max(2 * (wl.order // 2) + 1, min(wl.dims[0], nz_s))
+    dims_s, vel, src = sample(nz_s)
+    P, Pm, _ = oracle.run(vel, wl.h, wl.dt, wl.order, args.warmup, src, nthreads=cores)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        P, Pm, _ = oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, P0=P, Pm1=Pm, nthreads=cores)
+    oracle.run(vel, wl.h, wl.dt, wl.order, args.steps, src, P0=P, Pm1=Pm, nthreads=cores)
     el = time.perf_counter() - t0
     npts = int(np.prod(dims_s))
     value = npts * args.steps / el / 1e9
-    sample = f"{wl.name}: {nz_s} of {wl.dims[0]} planes ({dims_s}), 1 time step per bench step"
+    desc = (f"{wl.name}: {nz_s} of {wl.dims[0]} planes {dims_s}, {args.steps} steps in one oracle call, "
+            f"{cores} threads")
     line = {
         "impl": "reference", "metric": "grid-point updates/s (Gpts/s)", "value": value, "unit": "Gpts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
                    "sample_grid": list(dims_s)},
-        "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -407,6 +418,7 @@ def main(argv=None):
     ap.add_argument("--tsteps", type=int, default=1, choices=[1, 2],
                     help="2: temporal blocking, one launch per two steps (10 B per update)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -173,9 +173,10 @@ static TileCfg make_tb2() {
 }
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = {
-        make_tb2<1, 64, 16, 2, 1, 2, 2, 256>(), make_tb2<1, 64, 16, 3, 2, 2, 2, 128>(),
-        make_tb2<1, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<1, 128, 16, 3, 2, 1, 1, 256>(),
-        make_tb2<2, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<2, 64, 16, 4, 2, 1, 1, 128>()};
+        make_tb2<1, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<1, 64, 32, 2, 2, 1, 1, 256>(),
+        make_tb2<1, 64, 32, 2, 1, 1, 1, 512>(), make_tb2<1, 128, 16, 2, 2, 1, 1, 256>(),
+        make_tb2<1, 64, 16, 3, 2, 1, 1, 128>(),
+        make_tb2<2, 64, 16, 2, 1, 1, 1, 256>(), make_tb2<2, 64, 32, 2, 2, 1, 1, 256>()};
     return t;
 }
 

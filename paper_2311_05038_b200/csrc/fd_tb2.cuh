@@ -118,6 +118,28 @@ tb2_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box
     // this thread's work items (fixed for every plane)
     constexpr int NIA = (C::ITEMS_A + C::NCONS - 1) / C::NCONS;
     constexpr int NIB = (C::ITEMS_B + C::NCONS - 1) / C::NCONS;
+    int qA[NIA], reA[NIA], xbA[NIA];
+    uint32_t inxA[NIA];                  // bit e: x term included for point e
+#pragma unroll
+    for (int ii = 0; ii < NIA; ++ii) {
+        const int it = min(tid + ii * C::NCONS, C::ITEMS_A - 1);
+        qA[ii] = it % C::QXE;
+        reA[ii] = (it / C::QXE) * C::NYA;
+        xbA[ii] = x0 - 4 + 4 * qA[ii];
+        inxA[ii] = 0;
+        for (int e = 0; e < 4; ++e) inxA[ii] |= (uint32_t)((xbA[ii] + e >= R) && (xbA[ii] + e < nx - R)) << e;
+    }
+    int qB[NIB], riB[NIB], xbB[NIB];
+    uint32_t inxB[NIB];
+#pragma unroll
+    for (int ii = 0; ii < NIB; ++ii) {
+        const int it = min(tid + ii * C::NCONS, C::ITEMS_B - 1);
+        qB[ii] = it % C::QXI + 1;
+        riB[ii] = (it / C::QXI) * C::NYB;
+        xbB[ii] = x0 + 4 * (qB[ii] - 1);
+        inxB[ii] = 0;
+        for (int e = 0; e < 4; ++e) inxB[ii] |= (uint32_t)((xbB[ii] + e >= R) && (xbB[ii] + e < nx - R)) << e;
+    }
 
     for (int l = 2 * R; l < nload; ++l) {
         const int j = z0 - 2 * R + l, z1 = j - R, a = l - 2 * R;
@@ -140,14 +162,11 @@ tb2_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box
                 for (int q = 0; q < prm.nsrc; ++q) srcs_here |= ((smask >> q) & 1u) && prm.sz[q] == z1;
 #pragma unroll
             for (int ii = 0; ii < NIA; ++ii) {
-                const int it = tid + ii * C::NCONS;
-                if (it >= C::ITEMS_A) break;
-                const int q = it % C::QXE, g = it / C::QXE;
-                const int re0 = g * C::NYA;                       // first E row
-                const int xb = x0 - 4 + 4 * q;                    // first x of the quad
+                if (tid + ii * C::NCONS >= C::ITEMS_A) break;
+                const int q = qA[ii], re0 = reA[ii], xb = xbA[ii];   // quad, first E row, first x
                 bool inx[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+                for (int e = 0; e < 4; ++e) inx[e] = (inxA[ii] >> e) & 1u;
                 float4 col[C::NYA + 2 * R];
 #pragma unroll
                 for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
@@ -233,14 +252,11 @@ tb2_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box
                 for (int q = 0; q < prm.nsrc; ++q) srcs_here |= ((smask >> q) & 1u) && prm.sz[q] == z2;
 #pragma unroll
             for (int ii = 0; ii < NIB; ++ii) {
-                const int it = tid + ii * C::NCONS;
-                if (it >= C::ITEMS_B) break;
-                const int qi = it % C::QXI, g = it / C::QXI;
-                const int q = qi + 1, ri0 = g * C::NYB;
-                const int xb = x0 + 4 * qi;
+                if (tid + ii * C::NCONS >= C::ITEMS_B) break;
+                const int q = qB[ii], ri0 = riB[ii], xb = xbB[ii];
                 bool inx[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+                for (int e = 0; e < 4; ++e) inx[e] = (inxB[ii] >> e) & 1u;
                 float4 col[C::NYB + 2 * R];
 #pragma unroll
                 for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
