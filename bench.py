@@ -281,8 +281,7 @@ def run_ours(args, wl):
     opts = {fd.FD_OPT_ASYNC: 1}
     if args.no_graph:
         opts[fd.FD_OPT_GRAPH] = 0
-    if args.tsteps == 2:
-        opts[fd.FD_OPT_TSTEPS] = 2
+    opts[fd.FD_OPT_TSTEPS] = args.tsteps
     sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts)
     sim.step(args.warmup)
     # setup for the timed steps (trace/wavelet tables for both passes, the CUDA
@@ -364,7 +363,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     k_avg_s = kms / kn / 1e3
     # algorithmic bytes per launch: 16 B per point for a one-step launch; a
     # temporal-blocking launch does two steps for 20 B per point
-    steps_per_launch = 2 if args.tsteps == 2 else 1
+    steps_per_launch = int(info.get("steps_per_launch", 1) or 1)
     bytes_per_launch = (20.0 if steps_per_launch == 2 else BYTES_PER_POINT) * wl.npts
     achieved = bytes_per_launch / k_avg_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -373,7 +372,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
             "algorithmic_bytes_per_point": bytes_per_launch / wl.npts / steps_per_launch,
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
             "points_per_launch": wl.npts,
-            "kernel": ("tb2_step_kernel" if steps_per_launch == 2 else "fused_step_kernel") if wl.ndim == 3
+            "kernel": ("tb2ws_step_kernel" if steps_per_launch == 2 else "fused_step_kernel") if wl.ndim == 3
             else "tile2d_step_kernel",
             "kernel_ms_per_launch": k_avg_s * 1e3, "kernel_share_of_step": min(1.0, k_avg_s * 1e3 / (ms_step * steps_per_launch)),
             "kernel_times_ms": {k: v[0] for k, v in ktimes.items()},
@@ -415,8 +414,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="plain launches instead of CUDA-graph replay")
     ap.add_argument("--clock-sampler", default="nvml", choices=["nvml", "smi"])
-    ap.add_argument("--tsteps", type=int, default=1, choices=[1, 2],
-                    help="2: temporal blocking, one launch per two steps (10 B per update)")
+    ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2],
+                    help="0 auto (library default), 1 one step per launch, 2 temporal blocking (10 B/update)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     args = ap.parse_args(argv)

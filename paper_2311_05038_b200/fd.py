@@ -52,7 +52,7 @@ class FdInfo(ctypes.Structure):
                 ("tile_y", ctypes.c_int), ("rows_per_thread", ctypes.c_int), ("p_stages", ctypes.c_int),
                 ("k_stages", ctypes.c_int), ("ctas", ctypes.c_int), ("threads_per_cta", ctypes.c_int),
                 ("smem_bytes", ctypes.c_int), ("zchunks", ctypes.c_int), ("order", ctypes.c_int),
-                ("device_bytes", ctypes.c_double)]
+                ("device_bytes", ctypes.c_double), ("steps_per_launch", ctypes.c_int)]
 
     def as_dict(self) -> dict:
         d = {}

@@ -19,7 +19,7 @@ for spec in "C3 2" "C3 8" "C2 2" "C2 8"; do
 done
 # temporal blocking (two steps per launch), 3D order 2 and 4
 for ord in 2 4; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tb2_step -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tb2 -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_C3_o${ord}_tb2 -f \
       python bench.py --config C3 --order $ord --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --tsteps 2 > gpurun_out/ncu_full_C3_o${ord}_tb2.log 2>&1
 done

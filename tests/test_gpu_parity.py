@@ -395,7 +395,7 @@ def test_temporal_blocking_bitwise(fd, oracle, dims, order):
     recs = [tuple(d // 2 for d in dims), (dims[0] // 3, 15, 63), (dims[0] - 3, 17, 5), (1, 1, 1)]
     ref = run_gpu(fd, vel, h, dt, order, 41, src, recs)
     ntb = 0
-    for tile in range(8):
+    for tile in range(16):
         for zc in (0, 1, 3):
             for graph in (1, 0):
                 try:
