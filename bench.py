@@ -376,6 +376,10 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
             else "tile2d_step_kernel",
             "kernel_ms_per_launch": k_avg_s * 1e3, "kernel_share_of_step": min(1.0, k_avg_s * 1e3 / (ms_step * steps_per_launch)),
             "kernel_times_ms": {k: v[0] for k, v in ktimes.items()},
+            # the Gpts/s ceiling of this kernel's data movement at `peak`, and the
+            # value against the one-step-per-launch (16 B/update) ceiling
+            "gpts_ceiling": peak / (bytes_per_launch / wl.npts / steps_per_launch),
+            "value_over_single_step_ceiling": gpts * BYTES_PER_POINT / peak / world,
             "kernel_time_source": "CUDA events around every launch, a second pass of K steps"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

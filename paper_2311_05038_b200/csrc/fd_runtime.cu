@@ -171,12 +171,29 @@ static TileCfg make_tb2ws() {
     return TileCfg{3, R, TX, TY, NYB, DP, DA, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES,
                    (const void *)tb2ws_step_kernel<C>, launch_tb2ws<C>};
 }
+template <class C>
+static void launch_tb2d(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
+                        const CUtensorMap &c, const StepParams &p) {
+    tb2d_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
+}
+template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1>
+static TileCfg make_tb2d() {
+    using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB>;
+    return TileCfg{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES,
+                   (const void *)tb2d_step_kernel<C>, launch_tb2d<C>};
+}
+
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = {
         // r01 sweep (C3, order 2): 513 / 444 / 425 / 418 Gpts/s
         make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 64, 16, 3, 4, 2, 2, 2>(),
         make_tb2ws<1, 64, 16, 2, 4, 1, 1, 1, 2>(), make_tb2ws<1, 64, 16, 2, 2, 2, 2, 2, 2>(),
-        make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>()};
+        make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
+        // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows
+        make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
+        make_tb2d<2, 64, 28, 4, 4, 3, 2>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
+        make_tb2d<3, 64, 26, 4, 2, 3, 2>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
+        make_tb2d<4, 64, 24, 4, 4, 3, 2>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>()};
     return t;
 }
 
@@ -763,12 +780,12 @@ static fd_status prepare(fd_ctx *c) {
                          c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
     }
     if (c->opt_tsteps == 2) {
-        // temporal blocking: 3D, r <= 2, one slab, fused path
-        if (c->ndim != 3 || c->R > 2 || c->slabs.size() != 1 || c->nranks != 1 || c->opt_kernel != 0)
-            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs a 3D single-slab context with r <= 2 and the fused kernel");
+        // temporal blocking: 3D r <= 2 or 2D, one slab, fused path
+        if ((c->ndim == 3 && c->R > 2) || c->slabs.size() != 1 || c->nranks != 1 || c->opt_kernel != 0)
+            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs a single-slab context (3D: r <= 2) and the fused kernel");
         const auto &tb = tb2_table();
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
-            if (tb[i].r != c->R || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
+            if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
             const int occ = occupancy(tb[i]);
             if (occ > 0) { c->tb2 = i; c->tb2occ = occ; }
         }
@@ -785,12 +802,16 @@ static fd_status prepare(fd_ctx *c) {
         }
         const TileCfg &ts = tile_table()[c->tile];
         const int64_t planes = s.nz + 2 * c->R;
-        bool ok = make_map(&s.mKe, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, t.tbz, 1);
+        // 3D boxes (x, y rows, 1 plane); 2D boxes (x, 1, z rows)
+        const bool d3 = c->ndim == 3;
+        const int py = d3 ? t.pbz : 1, pz = d3 ? 1 : t.pbz, ey = d3 ? t.tbz : 1, ez = d3 ? 1 : t.tbz;
+        const int sy = d3 ? ts.ty + 2 * c->R : 1, sz = d3 ? 1 : ts.pbz, ty1 = d3 ? ts.ty : 1, tz1 = d3 ? 1 : ts.tbz;
+        bool ok = make_map(&s.mKe, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, ey, ez);
         for (int b = 0; b < 4 && ok; ++b)
-            ok = make_map(&s.mP0[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, t.pbz, 1) &&
-                 make_map(&s.mPm[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, t.tbz, 1) &&
-                 make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.pbw, ts.ty + 2 * c->R, 1) &&
-                 make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.tbw, ts.ty, 1);
+            ok = make_map(&s.mP0[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, py, pz) &&
+                 make_map(&s.mPm[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, ey, ez) &&
+                 make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.pbw, sy, sz) &&
+                 make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.tbw, ty1, tz1);
         if (!ok) {
             c->poisoned = true;
             return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed (temporal blocking)");
@@ -1499,8 +1520,8 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         return FD_OK;
     case FD_OPT_TSTEPS:
         if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_TSTEPS must be 0 (auto), 1 or 2");
-        if (v == 2 && (c->ndim != 3 || c->R > 2))
-            return fail(FD_ERR_ARG, "FD_OPT_TSTEPS=2 is implemented for 3D grids with order <= 4");
+        if (v == 2 && c->ndim == 3 && c->R > 2)
+            return fail(FD_ERR_ARG, "FD_OPT_TSTEPS=2 is implemented for 2D grids and 3D grids with order <= 4");
         c->opt_tsteps = (int)v;
         return FD_OK;
     case FD_OPT_TB2TILE:

@@ -376,4 +376,244 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     }
 }
 
+
+// ------------------------------------------------------------------ 2D two-step kernel
+// 2D grids stream TY-row blocks down z (as tile2d_step_kernel).  Per block the
+// producer loads ONE stage: the P^k box (TX+16) x (TY+4r) rows and the grown
+// (P^{k-1}, K) boxes (TX+8) x (TY+2r); stage-A warps compute P^{k+1} on the
+// grown block into a shared P1 tile (interior rows to C), stage-B warps
+// compute P^{k+2} on the block from it (to D), one block behind.  Blocks are
+// self-contained (their z halo rows come with the box), so the P1 ring only
+// decouples A from B.  20 B per point per launch = 10 B per update.
+template <int R_, int TX_, int TY_, int NYA_, int NYB_, int NS_, int N1_, int MINB_ = 1>
+struct CfgWS2 {
+    static constexpr int R = R_, TX = TX_, TY = TY_, NYA = NYA_, NYB = NYB_, NS = NS_, N1 = N1_, MINB = MINB_;
+    static constexpr int BX0 = TX + 16, BY0 = TY + 4 * R;         // P^k block (x halo 8, z halo 2r)
+    static constexpr int BXE = TX + 8, BYE = TY + 2 * R;          // grown block E
+    static constexpr int QXE = BXE / 4, QXI = TX / 4;
+    static constexpr int NTA = QXE * (BYE / NYA), NTB = QXI * (TY / NYB);
+    static constexpr int NWA = (NTA + 31) / 32, NWB = (NTB + 31) / 32;
+    static constexpr int NTHREADS = 32 * (NWA + NWB + 1);
+    static constexpr int P0F = (BX0 * BY0 + 31) / 32 * 32;
+    static constexpr int EF = (BXE * BYE + 31) / 32 * 32;
+    static constexpr int STAGE = P0F + 2 * EF;                    // [P^k | P^{k-1} | K]
+    static constexpr uint32_t STAGE_BYTES = (BX0 * BY0 + 2 * BXE * BYE) * 4;
+    static constexpr int SMEM_BYTES = (NS * STAGE + N1 * EF) * 4 + (2 * NS + 2 * N1) * 8 + 16;
+    static constexpr int NY = NYB, DP = NS, DA = N1;
+    static_assert(BYE % NYA == 0 && TY % NYB == 0, "tile");
+    static_assert(BX0 <= 256 && BY0 <= 256 && R <= 4, "TMA box");
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
+tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box (BX0, 1, BY0)
+                 const __grid_constant__ CUtensorMap map_pm,   // P^{k-1} buffer, box (BXE, 1, BYE)
+                 const __grid_constant__ CUtensorMap map_k,    // K, box (BXE, 1, BYE)
+                 const StepParams prm) {
+    constexpr int R = C::R;
+    extern __shared__ __align__(128) float smem[];
+    float *sSt = smem;
+    float *sP1 = smem + C::NS * C::STAGE;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sP1 + C::N1 * C::EF);
+    uint64_t *fullS = bars, *emptyS = fullS + C::NS, *full1 = emptyS + C::NS, *empty1 = full1 + C::N1;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int unit = blockIdx.x;
+    const int chunk = unit / prm.ntx;
+    const int x0 = (unit - chunk * prm.ntx) * C::TX;
+    const int span = prm.zhi - prm.zlo;
+    const int nb = (span + C::TY - 1) / C::TY;
+    const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
+    const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
+    if (tid == 0) {
+        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], C::NWA + C::NWB); }
+        for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], C::NWA); mbar_init(&empty1[i], C::NWB); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (b1 <= b0) return;
+    const int nload = b1 - b0;
+    const int64_t nx = prm.nx;
+    const int64_t kk = step_index(prm);
+    constexpr float c0 = tap(R, 0);
+    int rp = prm.rec.off ? prm.rec.off[unit] : 0;
+    const int rend = prm.rec.off ? prm.rec.off[unit + 1] : 0;
+
+    if (warp == C::NWA + C::NWB) {
+        if (lane == 0) {
+            tma_prefetch_desc(&map_p0); tma_prefetch_desc(&map_pm); tma_prefetch_desc(&map_k);
+            for (int l = 0; l < nload; ++l) {
+                const int s = l % C::NS, rb = prm.zlo + (b0 + l) * C::TY;
+                mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
+                mbar_expect_tx(&fullS[s], C::STAGE_BYTES);
+                float *st = sSt + s * C::STAGE;
+                tma_load_3d(st, &map_p0, &fullS[s], x0 - 8, 0, rb - 2 * R + R);        // rows rb-2r.. (+r halo)
+                tma_load_3d(st + C::P0F, &map_pm, &fullS[s], x0 - 4, 0, rb - R + R);   // rows rb-r..
+                tma_load_3d(st + C::P0F + C::EF, &map_k, &fullS[s], x0 - 4, 0, rb - R);
+            }
+        }
+        return;
+    }
+
+    if (warp < C::NWA) {
+        // ---------------------------------------------------------------- stage A
+        const bool act = tid < C::NTA;
+        const int q = act ? tid % C::QXE : 0, re0 = act ? (tid / C::QXE) * C::NYA : 0;
+        const int xb = x0 - 4 + 4 * q;
+        bool inx[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+        const bool qint = q >= 1 && q <= C::QXI;
+        uint32_t smask = 0;
+        for (int s2 = 0; s2 < prm.nsrc; ++s2)
+            if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
+        float *const trow = trace_row_of(prm, kk);
+        const float *const wv = w_next_of(prm, kk);
+        for (int l = 0; l < nload; ++l) {
+            const int s = l % C::NS, s1 = l % C::N1;
+            const int rb = prm.zlo + (b0 + l) * C::TY;
+            mbar_wait(&fullS[s], (l / C::NS) & 1);
+            mbar_wait(&empty1[s1], ((l / C::N1) & 1) ^ 1);
+            const float *tp = sSt + s * C::STAGE, *tpm = tp + C::P0F, *tk = tpm + C::EF;
+            float *t1 = sP1 + s1 * C::EF;
+            if (act) {
+                float4 col[C::NYA + 2 * R];
+#pragma unroll
+                for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tp + (re0 + i) * C::BX0 + 4 * q + 4);
+#pragma unroll
+                for (int yy = 0; yy < C::NYA; ++yy) {
+                    const int re = re0 + yy, z = rb - R + re;
+                    const float *row = tp + (re + R) * C::BX0 + 4 * q;
+                    const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
+                    const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                    const int offe = re * C::BXE + 4 * q;
+                    const float4 pm4 = lds128(tpm + offe), k4 = lds128(tk + offe);
+                    const int64_t gz = prm.gz0 + z;
+                    const bool inz = (gz >= R) && (gz < prm.nzg - R);
+                    float4 o;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float pc = av[4 + e];
+                        float sx = __fmul_rn(c0, pc);
+#pragma unroll
+                        for (int m = 1; m <= R; ++m) sx = __fmaf_rn(tap(R, m), __fadd_rn(av[4 + e - m], av[4 + e + m]), sx);
+                        float S = inx[e] ? sx : 0.f;
+                        float szz = __fmul_rn(c0, pc);
+#pragma unroll
+                        for (int m = 1; m <= R; ++m)
+                            szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
+                        S = inz ? __fadd_rn(S, szz) : S;
+                        f4set(o, e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pm4, e))));
+                    }
+                    const bool interior = qint && re >= R && re < R + C::TY && z < prm.zhi;
+                    if (interior && trow) {                            // raw P^{k+1}, owner only
+                        for (int r2 = rp; r2 < rend && prm.rec.z[r2] <= z; ++r2) {
+                            if (prm.rec.z[r2] != z) continue;
+                            const int dx = prm.rec.x[r2] - xb;
+                            if (dx >= 0 && dx < 4) trow[prm.rec.id[r2]] = f4(o, dx);
+                        }
+                    }
+                    if (smask) {                                       // w_{k+1} wherever in E
+                        for (int s2 = 0; s2 < prm.nsrc; ++s2) {
+                            if (!((smask >> s2) & 1u) || prm.sz[s2] != z) continue;
+                            const int dx = prm.sx[s2] - xb;
+                            f4set(o, dx, __fadd_rn(f4(o, dx), wv[s2]));
+                        }
+                    }
+                    *reinterpret_cast<float4 *>(t1 + offe) = o;
+                    if (interior && xb < prm.pitch)
+                        *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + R) * prm.pitch + xb) = o;
+                }
+            }
+            while (rp < rend && prm.rec.z[rp] < rb + C::TY) ++rp;
+            __syncwarp();
+            if (lane == 0) { mbar_arrive(&full1[s1]); mbar_arrive(&emptyS[s]); }
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------------- stage B
+    const int tb = tid - 32 * C::NWA;
+    const bool act = tb < C::NTB;
+    const int qi = act ? tb % C::QXI : 0, ri0 = act ? (tb / C::QXI) * C::NYB : 0;
+    const int q = qi + 1, xb = x0 + 4 * qi;
+    bool inx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    uint32_t smask = 0;
+    for (int s2 = 0; s2 < prm.nsrc; ++s2)
+        if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
+    float *const trow = trace_row_of(prm, kk + 1);
+    const float *const wv = w_next_of(prm, kk + 1);
+    for (int l = 0; l < nload; ++l) {
+        const int s = l % C::NS, s1 = l % C::N1;
+        const int rb = prm.zlo + (b0 + l) * C::TY;
+        mbar_wait(&full1[s1], (l / C::N1) & 1);
+        const float *tp = sSt + s * C::STAGE, *tk = tp + C::P0F + C::EF;
+        const float *t1 = sP1 + s1 * C::EF;
+        const int zt = rb + ri0;
+        float4 out[C::NYB];
+        if (act) {
+            float4 col[C::NYB + 2 * R];
+#pragma unroll
+            for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1 + (ri0 + i) * C::BXE + 4 * q);
+#pragma unroll
+            for (int yy = 0; yy < C::NYB; ++yy) {
+                const int re = ri0 + yy + R;
+                const int offe = re * C::BXE + 4 * q;
+                const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
+                const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4), k4 = lds128(tk + offe);
+                const int64_t gz = prm.gz0 + zt + yy;
+                const bool inz = (gz >= R) && (gz < prm.nzg - R);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float pc = av[4 + e];
+                    float sx = __fmul_rn(c0, pc);
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) sx = __fmaf_rn(tap(R, m), __fadd_rn(av[4 + e - m], av[4 + e + m]), sx);
+                    float S = inx[e] ? sx : 0.f;
+                    float szz = __fmul_rn(c0, pc);
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+                        szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
+                    S = inz ? __fadd_rn(S, szz) : S;
+                    f4set(out[yy], e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pk4, e))));
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&empty1[s1]); mbar_arrive(&emptyS[s]); }
+        if (!act) continue;
+        for (int r2 = rp; r2 < rend && prm.rec.z[r2] < rb + C::TY; ++r2) {
+            const int dz = prm.rec.z[r2] - zt, dx = prm.rec.x[r2] - xb;
+            if (dz >= 0 && dz < C::NYB && dx >= 0 && dx < 4 && trow) {
+#pragma unroll
+                for (int yy = 0; yy < C::NYB; ++yy)
+                    if (yy == dz) trow[prm.rec.id[r2]] = f4(out[yy], dx);
+            }
+        }
+        while (rp < rend && prm.rec.z[rp] < rb + C::TY) ++rp;
+        if (smask) {
+            for (int s2 = 0; s2 < prm.nsrc; ++s2) {
+                if (!((smask >> s2) & 1u)) continue;
+                const int dz = prm.sz[s2] - zt, dx = prm.sx[s2] - xb;
+                if (dz < 0 || dz >= C::NYB) continue;
+#pragma unroll
+                for (int yy = 0; yy < C::NYB; ++yy)
+                    if (yy == dz) {
+                        const float v = f4(out[yy], dx);
+                        prm.src_raw[s2] = v;
+                        f4set(out[yy], dx, __fadd_rn(v, wv[s2]));
+                    }
+            }
+        }
+        if (xb < prm.pitch) {
+            float *dst = prm.pnext2 + (int64_t)(zt + R) * prm.pitch + xb;
+#pragma unroll
+            for (int yy = 0; yy < C::NYB; ++yy)
+                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+        }
+    }
+}
+
 }  // namespace fdk

@@ -39,10 +39,21 @@ def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *
     rank, world = dist.get_rank(), dist.get_world_size()
     if nccl_id is None and world > 1:
         nccl_id = bootstrap_nccl_id()
-    return _fd.Simulation(vel_slab, h, dt, order, flags,
-                          dist={"global_dims": tuple(global_dims), "rank": rank, "nranks": world,
-                                "device": device, "nccl_id": nccl_id, "vel_is_slab": True},
-                          options=options, stream=stream)
+    sim, err = None, None
+    try:
+        sim = _fd.Simulation(vel_slab, h, dt, order, flags,
+                             dist={"global_dims": tuple(global_dims), "rank": rank, "nranks": world,
+                                   "device": device, "nccl_id": nccl_id, "vel_is_slab": True},
+                             options=options, stream=stream)
+    except _fd.FDError as e:
+        err = e
+    # every rank must have a context before anyone steps (NCCL is initialised
+    # collectively at the first fd_step): fail everywhere if one rank failed
+    if not all_ok(err is None):
+        if sim is not None:
+            sim.close()
+        raise err if err is not None else RuntimeError("fd_create_dist failed on another rank")
+    return sim
 
 
 def all_ok(ok: bool) -> bool:

@@ -74,6 +74,8 @@ def main(tag):
             continue
         wl, order, tb2 = m.group(1), int(m.group(2)), bool(m.group(3))
         d = raw(rep)
+        kname = d.get("Kernel Name", ("", ""))[0]
+        tb2 = tb2 or "tb2" in kname          # the default 3D order-2 path is two steps per launch
         rd = to_bytes(*d["dram__bytes_read.sum"])
         wr = to_bytes(*d["dram__bytes_write.sum"])
         npts = npts_of(wl)
@@ -85,6 +87,7 @@ def main(tag):
                                   "algorithmic_bytes": alg, "bytes_per_point": (rd + wr) / npts,
                                   "ncu_duration_s": dur_s, "tag": tag}
         lines += [f"## {wl}, order {order}{' (temporal blocking, 2 steps per launch)' if tb2 else ''}", "",
+                  f"* kernel: `{kname[:120]}`",
                   f"* DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB = {(rd + wr) / npts:.2f} B/pt "
                   f"(algorithmic {alg / npts:.0f} B/pt = {alg / 1e9:.3f} GB)",
                   f"* ncu duration {dur_s * 1e6:.1f} us -> {(rd + wr) / dur_s / 1e9:.0f} GB/s DRAM, "

@@ -445,3 +445,31 @@ def test_reserve_then_step_bitwise(fd):
             got = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
         for a, b in zip(got, ref[:3]):
             assert np.array_equal(a, b), ts
+
+
+@pytest.mark.parametrize("dims,order", [((90, 300), 2), ((131, 200), 4), ((75, 260), 6), ((64, 129), 8)])
+def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
+    from paper_2311_05038_b200 import fd as fdm
+    vel = _rand_vel(dims, seed=47)
+    h, dt = 10.0, 0.5e-3
+    src = [((dims[0] // 2, dims[1] // 2), 25.0, 0.02, 1.0), ((30 - order // 2, 64), 18.0, 0.03, -0.6),
+           ((dims[0] // 2, dims[1] // 2), 12.0, 0.04, 0.3)]
+    recs = [(dims[0] // 2, dims[1] // 2), (29, 63), (dims[0] - 3, 5), (1, 1), (60, 130 % dims[1])]
+    ref = run_gpu(fd, vel, h, dt, order, 41, src, recs, options={fd.FD_OPT_TSTEPS: 1})
+    ntb = 0
+    for tile in range(32):
+        for zc in (0, 1, 3):
+            for graph in (1, 0):
+                try:
+                    got = run_gpu(fd, vel, h, dt, order, 41, src, recs,
+                                  options={fd.FD_OPT_TSTEPS: 2, fdm.FD_OPT_TB2TILE: tile,
+                                           fd.FD_OPT_ZCHUNKS: zc, fd.FD_OPT_GRAPH: graph})
+                except fdm.FDError as e:
+                    assert e.status in (-1, -5, -7), e
+                    break
+                ntb += 1
+                for a, b in zip(got[:3], ref[:3]):
+                    assert np.array_equal(a, b), (tile, zc, graph)
+    assert ntb >= 2
+    Po, _, To = oracle.run(vel, h, dt, order, 41, src, recs)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
