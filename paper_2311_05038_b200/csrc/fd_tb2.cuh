@@ -83,9 +83,11 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     const int z0 = prm.zlo + (int)(((int64_t)span * chunk) / prm.nchunks);
     const int z1e = prm.zlo + (int)(((int64_t)span * (chunk + 1)) / prm.nchunks);
     if (tid == 0) {
-        for (int i = 0; i < C::NSP; ++i) { mbar_init(&fullP[i], 1); mbar_init(&emptyP[i], C::NWA + C::NWB); }
-        for (int i = 0; i < C::NSA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], C::NWA + C::NWB); }
-        for (int i = 0; i < C::NS1; ++i) { mbar_init(&full1[i], C::NWA); mbar_init(&empty1[i], C::NWB); }
+        // role barriers count every thread of the arriving warps: each thread
+        // releases its own shared-memory accesses (no reliance on __syncwarp)
+        for (int i = 0; i < C::NSP; ++i) { mbar_init(&fullP[i], 1); mbar_init(&emptyP[i], 32 * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::NSA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 32 * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::NS1; ++i) { mbar_init(&full1[i], 32 * C::NWA); mbar_init(&empty1[i], 32 * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -158,8 +160,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 // planes below z0 - r are z taps only: A is done with them now;
                 // planes z0 - r .. z0 - 1 still serve A's x-y taps (released there)
                 if (l < R) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&emptyP[s]);
+                    mbar_arrive(&emptyP[s]);
                 }
                 continue;
             }
@@ -175,6 +176,9 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             const int64_t gz = prm.gz0 + z1;
             const bool inz = (gz >= R) && (gz < prm.nzg - R);
             const bool store = (z1 >= z0) && (z1 < z1e);
+            float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
+#pragma unroll
+            for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (act) {
                 float4 col[C::NYA + 2 * R];
 #pragma unroll
@@ -209,13 +213,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         f4set(o, e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pm4, e))));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && y < ny;
-                    if (store && interior && rz == z1 && trow) {     // raw P^{k+1}, owner only
-                        for (int r2 = rp; r2 < rend && prm.rec.z[r2] == z1; ++r2) {
-                            if (prm.rec.y[r2] != y) continue;
-                            const int dx = prm.rec.x[r2] - xb;
-                            if (dx >= 0 && dx < 4) trow[prm.rec.id[r2]] = f4(o, dx);
-                        }
-                    }
+                    oraw[yy] = o;
                     if (smask) {                                      // w_{k+1} wherever in E
                         for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                             if (!((smask >> s2) & 1u) || prm.sz[s2] != z1 || prm.sy[s2] != y) continue;
@@ -228,14 +226,20 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + R) * ny + y) * prm.pitch + xb) = o;
                 }
             }
-            if (rz == z1) {
-                while (rp < rend && prm.rec.z[rp] <= z1) ++rp;
+            if (store && rz == z1) {                              // owners: tile-interior A threads
+                rp = warp_record<C::NYA>(oraw, prm.rec.z, prm.rec.id, rp, rend, z1, z1 + 1, trow,
+                                         [&](int i, int &ln, int &yy, int &e) {
+                                             const int re = prm.rec.y[i] - (y0 - R), dx = prm.rec.x[i] - (x0 - 4);
+                                             const int t = (re / C::NYA) * C::QXE + dx / 4;
+                                             if ((t >> 5) != warp) return false;
+                                             ln = t & 31; yy = re % C::NYA; e = dx & 3;
+                                             return true;
+                                         });
                 rz = rp < rend ? prm.rec.z[rp] : INT32_MAX;
             }
             // P1 plane z1 ready; P^k plane z1 done for A (x-y taps); aux plane z1
             // done for A; planes of P^k below the window are A-done at their read
-            __syncwarp();
-            if (lane == 0) {
+            {
                 mbar_arrive(&full1[s1]);
                 mbar_arrive(&emptyP[sz1]);
                 mbar_arrive(&emptyA[sa]);
@@ -279,8 +283,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             // warm-up: B never reads P^k loads 0 .. 2r-1 (it reads P^k at z2 >= z0,
             // load b + r >= 2r) nor aux planes 0 .. r-1; P1 planes 0 .. r-1 are z
             // taps only.  Release them as this iteration passes.
-            __syncwarp();
-            if (lane == 0) {
+            {
                 mbar_arrive(&emptyP[a % C::NSP]);
                 if (a < R) {
                     mbar_arrive(&empty1[s1]);
@@ -334,26 +337,23 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         }
         // release: P1 plane z2 (x-y taps done; its column is in the queue), P^k
         // plane z2 (pointwise), aux plane z2 (K)
-        __syncwarp();
-        if (lane == 0) {
+        {
             mbar_arrive(&empty1[sb1]);
             mbar_arrive(&emptyP[sp]);
             mbar_arrive(&emptyA[sab]);
         }
-        if (!act) continue;
-        if (rz <= z2) {
-            while (rp < rend && prm.rec.z[rp] < z2) ++rp;
-            for (int r2 = rp; r2 < rend && prm.rec.z[r2] == z2; ++r2) {
-                const int dy = prm.rec.y[r2] - (y0 + ri0), dx = prm.rec.x[r2] - xb;
-                if (dy >= 0 && dy < C::NYB && dx >= 0 && dx < 4) {
-#pragma unroll
-                    for (int yy = 0; yy < C::NYB; ++yy)
-                        if (yy == dy && trow) trow[prm.rec.id[r2]] = f4(out[yy], dx);
-                }
-            }
-            while (rp < rend && prm.rec.z[rp] <= z2) ++rp;
+        if (rz == z2) {                                           // owners: B threads
+            rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, z2, z2 + 1, trow,
+                                     [&](int i, int &ln, int &yy, int &e) {
+                                         const int dy = prm.rec.y[i] - y0, dx = prm.rec.x[i] - x0;
+                                         const int t = (dy / C::NYB) * C::QXI + dx / 4;
+                                         if (C::NWA + (t >> 5) != warp) return false;
+                                         ln = t & 31; yy = dy % C::NYB; e = dx & 3;
+                                         return true;
+                                     });
             rz = rp < rend ? prm.rec.z[rp] : INT32_MAX;
         }
+        if (!act) continue;
         if (smask) {
             for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                 if (!((smask >> s2) & 1u) || prm.sz[s2] != z2) continue;
@@ -425,8 +425,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
     const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
     if (tid == 0) {
-        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], C::NWA + C::NWB); }
-        for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], C::NWA); mbar_init(&empty1[i], C::NWB); }
+        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], 32 * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], 32 * C::NWA); mbar_init(&empty1[i], 32 * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -475,6 +475,9 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             mbar_wait(&empty1[s1], ((l / C::N1) & 1) ^ 1);
             const float *tp = sSt + s * C::STAGE, *tpm = tp + C::P0F, *tk = tpm + C::EF;
             float *t1 = sP1 + s1 * C::EF;
+            float4 oraw[C::NYA];                                   // raw P^{k+1} (receivers)
+#pragma unroll
+            for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (act) {
                 float4 col[C::NYA + 2 * R];
 #pragma unroll
@@ -505,13 +508,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         f4set(o, e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pm4, e))));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && z < prm.zhi;
-                    if (interior && trow) {                            // raw P^{k+1}, owner only
-                        for (int r2 = rp; r2 < rend && prm.rec.z[r2] <= z; ++r2) {
-                            if (prm.rec.z[r2] != z) continue;
-                            const int dx = prm.rec.x[r2] - xb;
-                            if (dx >= 0 && dx < 4) trow[prm.rec.id[r2]] = f4(o, dx);
-                        }
-                    }
+                    oraw[yy] = o;
                     if (smask) {                                       // w_{k+1} wherever in E
                         for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                             if (!((smask >> s2) & 1u) || prm.sz[s2] != z) continue;
@@ -524,9 +521,16 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + R) * prm.pitch + xb) = o;
                 }
             }
-            while (rp < rend && prm.rec.z[rp] < rb + C::TY) ++rp;
-            __syncwarp();
-            if (lane == 0) { mbar_arrive(&full1[s1]); mbar_arrive(&emptyS[s]); }
+            if (rp < rend && prm.rec.z[rp] < rb + C::TY)              // owners: block-interior A threads
+                rp = warp_record<C::NYA>(oraw, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
+                                         [&](int i, int &ln, int &yy, int &e) {
+                                             const int re = prm.rec.z[i] - (rb - R), dx = prm.rec.x[i] - (x0 - 4);
+                                             const int t = (re / C::NYA) * C::QXE + dx / 4;
+                                             if ((t >> 5) != warp) return false;
+                                             ln = t & 31; yy = re % C::NYA; e = dx & 3;
+                                             return true;
+                                         });
+            { mbar_arrive(&full1[s1]); mbar_arrive(&emptyS[s]); }
         }
         return;
     }
@@ -581,18 +585,17 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) { mbar_arrive(&empty1[s1]); mbar_arrive(&emptyS[s]); }
+        { mbar_arrive(&empty1[s1]); mbar_arrive(&emptyS[s]); }
+        if (rp < rend && prm.rec.z[rp] < rb + C::TY)                  // owners: B threads
+            rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
+                                     [&](int i, int &ln, int &yy, int &e) {
+                                         const int dz = prm.rec.z[i] - rb, dx = prm.rec.x[i] - x0;
+                                         const int t = (dz / C::NYB) * C::QXI + dx / 4;
+                                         if (C::NWA + (t >> 5) != warp) return false;
+                                         ln = t & 31; yy = dz % C::NYB; e = dx & 3;
+                                         return true;
+                                     });
         if (!act) continue;
-        for (int r2 = rp; r2 < rend && prm.rec.z[r2] < rb + C::TY; ++r2) {
-            const int dz = prm.rec.z[r2] - zt, dx = prm.rec.x[r2] - xb;
-            if (dz >= 0 && dz < C::NYB && dx >= 0 && dx < 4 && trow) {
-#pragma unroll
-                for (int yy = 0; yy < C::NYB; ++yy)
-                    if (yy == dz) trow[prm.rec.id[r2]] = f4(out[yy], dx);
-            }
-        }
-        while (rp < rend && prm.rec.z[rp] < rb + C::TY) ++rp;
         if (smask) {
             for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                 if (!((smask >> s2) & 1u)) continue;
