@@ -185,9 +185,11 @@ static TileCfg make_tb2d() {
 
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = {
-        // r01 sweep (C3, order 2): 513 / 444 / 425 / 418 Gpts/s
+        // r01/r03 sweeps (C3, order 2): 504-516 / 444 / 425 / 418 Gpts/s; none of
+        // (64x8, 32x16, 128x8, deeper rings) beat the first
         make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 64, 16, 3, 4, 2, 2, 2>(),
         make_tb2ws<1, 64, 16, 2, 4, 1, 1, 1, 2>(), make_tb2ws<1, 64, 16, 2, 2, 2, 2, 2, 2>(),
+        make_tb2ws<1, 64, 16, 2, 4, 3, 3, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
         make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
         // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows
         // (r01 sweep, C2: order 2 439 Gpts/s vs 376 single-step; order 4 368; order 8 239 vs 347)

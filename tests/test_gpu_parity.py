@@ -473,3 +473,62 @@ def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     assert ntb >= 2
     Po, _, To = oracle.run(vel, h, dt, order, 41, src, recs)
     assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# Full BASELINE sizes, in the launch configuration bench.py times (default
+# options): the GPU field after k steps is compared with the oracle on the
+# sub-grid that holds the discrete light cone (radius r*k around the source,
+# plus the real boundary where the cone meets it); outside it the GPU field
+# and traces must be exactly 0 (the property holds at any size).
+# ---------------------------------------------------------------------------
+def _cone_case(fd, oracle, wl, k):
+    # the workload's receivers plus a line through the source region: within k
+    # steps the physical wave (0.2-0.45 cells/step) only reaches nearby points;
+    # far receivers see the discrete cone's tail (~1e-60 in fp64, 0 in fp32),
+    # which the relative L2 over the whole matrix weighs at ~0
+    r = wl.order // 2
+    vel = wl.vel()
+    src = [(s.idx, s.f, s.t0, s.amp) for s in wl.sources]
+    c = wl.sources[0].idx
+    near = [tuple(c[:-1]) + (x,) for x in range(max(0, c[-1] - 30), min(wl.dims[-1], c[-1] + 31))]
+    receivers = list(wl.receivers) + near
+    wl = type(wl)(**{**wl.__dict__, "receivers": receivers})
+    with fd.Simulation(vel, wl.h, wl.dt, wl.order) as sim:
+        for s in wl.sources:
+            sim.add_source(s.idx, s.f, s.t0, s.amp)
+        sim.set_receivers(wl.receivers)
+        sim.step(k)
+        P = sim.wavefield()
+        T = sim.traces()
+        info = sim.info()
+    m = r * k + r + 1
+    lo = [max(0, c - m) for c in wl.sources[0].idx]
+    hi = [min(n, c + m + 1) for c, n in zip(wl.sources[0].idx, wl.dims)]
+    box = tuple(slice(a, b) for a, b in zip(lo, hi))
+    sub_src = [(tuple(i - a for i, a in zip(s[0], lo)), s[1], s[2], s[3]) for s in src]
+    inside = [j for j, q in enumerate(wl.receivers) if all(a <= i < b for i, a, b in zip(q, lo, hi))]
+    sub_rec = [tuple(i - a for i, a in zip(wl.receivers[j], lo)) for j in inside]
+    Po, _, To = oracle.run(vel[box], wl.h, wl.dt, wl.order, k, sub_src, sub_rec, nthreads=oracle.max_threads())
+    assert rel_l2(P[box], Po) <= TOL
+    outside = np.ones(P.shape, bool)
+    outside[box] = False
+    assert not P[outside].any()
+    assert rel_l2(T[inside], To) <= TOL
+    assert np.linalg.norm(To[-len(near):]) > 0.5 * np.linalg.norm(To)   # the near line carries the signal
+    others = np.setdiff1d(np.arange(len(wl.receivers)), inside)
+    assert not T[others].any()
+    return info
+
+
+@pytest.mark.parametrize("order,k", [(2, 100), (8, 30)])
+def test_full_size_c3_light_cone(fd, oracle, order, k):
+    from workloads import config
+    info = _cone_case(fd, oracle, config("C3", order=order), k)
+    assert info["steps_per_launch"] == (2 if order == 2 else 1)
+
+
+@pytest.mark.parametrize("order,k", [(2, 300), (8, 120)])
+def test_full_size_c2_light_cone(fd, oracle, order, k):
+    from workloads import config
+    _cone_case(fd, oracle, config("C2", order=order), k)
