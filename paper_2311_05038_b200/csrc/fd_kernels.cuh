@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace fdk {
 
 constexpr int kMaxSources = 16;
@@ -88,6 +90,15 @@ __device__ __forceinline__ float *trace_row_of(const StepParams &p, int64_t k) {
 }
 __device__ __forceinline__ const float *w_next_of(const StepParams &p, int64_t k) {
     return p.wtab + (k + 1) * p.nsrc;   // w_{k+1}
+}
+
+// compile-time loop: f(std::integral_constant<int, B>) ... f(<E-1>)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
 }
 
 // ------------------------------------------------------------------ PTX glue
@@ -289,7 +300,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     const int tx = tid % C::NTX, ty = tid / C::NTX;
     const int xb = x0 + 4 * tx;                   // first of this thread's 4 x points
     const int yb = y0 + ty * C::NY;               // first of its NY rows
-    const int64_t nx = prm.nx, ny = prm.ny;
+    const int nx = (int)prm.nx, ny = (int)prm.ny;   // 32-bit index math (dims <= 2^30)
     const int cL = C::pcol(4 * tx), cM = C::pcol(4 * tx + 4), cR = C::pcol(4 * tx + 8);
 
     bool inx[4];
@@ -320,25 +331,27 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     constexpr float c0 = tap(R, 0);
+    constexpr int Q = 2 * R + 1;
 
-    for (int l = 0; l < nload; ++l) {
+    // One plane of the stream.  For r <= 2 the register queue rotates instead
+    // of shifting: at phase PH (= l mod Q, a compile-time constant) the logical
+    // queue entry i (plane j - 2r + i) lives in q[(PH + i) % Q], so no register
+    // moves are spent per plane (a shift costs 2r MOVs per point).
+    auto plane = [&](const int l, auto ph) {
+        constexpr int PH = decltype(ph)::value;
         const int j = z0 - R + l;
         const int s = l % C::NSP;
         mbar_wait(&fullP[s], (l / C::NSP) & 1);
         const float *tp = sP + s * C::P_FLOATS;
-        // shift the register queue and append this thread's column of plane j
-#pragma unroll
-        for (int i = 0; i < 2 * R; ++i)
-#pragma unroll
-            for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = q[i + 1][yy];
+        // append this thread's column of plane j (logical entry 2r)
 #pragma unroll
         for (int yy = 0; yy < C::NY; ++yy)
-            q[2 * R][yy] = lds128(tp + (ty * C::NY + yy + C::HY) * C::BX + cM);
+            q[(PH + 2 * R) % Q][yy] = lds128(tp + (ty * C::NY + yy + C::HY) * C::BX + cM);
         if (j < z0 || j >= z1) {               // z-taps only: slot free now
             __syncwarp();
             if (lane == 0) mbar_arrive(&emptyP[s]);
         }
-        if (l < 2 * R) continue;
+        if (l < 2 * R) return;
 
         const int z = j - R;                       // plane computed now
         const int sz_ = (l - R) % C::NSP;          // its p tile (x-y taps)
@@ -346,8 +359,8 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         const int kl = l - 2 * R, ks = kl % C::NSK;
         mbar_wait(&fullK[ks], (kl / C::NSK) & 1);
         const float *tk = sK + ks * C::K_FLOATS;
-        const int64_t gz = prm.gz0 + z;
-        const bool inz = (gz >= R) && (gz < prm.nzg - R);
+        const int gz = (int)prm.gz0 + z;
+        const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
 
         float4 col[C::NY + 2 * C::HY];
         if (C::NDIM == 3) {
@@ -359,7 +372,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 #pragma unroll
         for (int yy = 0; yy < C::NY; ++yy) {
             const float *row = tz + (ty * C::NY + yy + C::HY) * C::BX;
-            const float4 L4 = lds128(row + cL), M4 = q[R][yy], R4 = lds128(row + cR);
+            const float4 L4 = lds128(row + cL), M4 = q[(PH + R) % Q][yy], R4 = lds128(row + cR);
             const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w,
                                  R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
@@ -383,7 +396,8 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                 float szz = __fmul_rn(c0, pc);
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
-                    szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(q[R - m][yy], e), f4(q[R + m][yy], e)), szz);
+                    szz = __fmaf_rn(tap(R, m),
+                                    __fadd_rn(f4(q[(PH + R - m) % Q][yy], e), f4(q[(PH + R + m) % Q][yy], e)), szz);
                 S = inz ? __fadd_rn(S, szz) : S;
                 const float upd = __fmaf_rn(f4(kk4, e), S, __fmaf_rn(2.f, pc, -f4(pp4, e)));
                 f4set(out[yy], e, upd);
@@ -422,11 +436,29 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             }
         }
         // store p_next in place of p_prev (float4; rows outside the grid skipped)
-        if (xb < prm.pitch) {
+        if (xb < (int)prm.pitch) {
             float *dst = prm.pnext + ((int64_t)(z + R) * ny + yb) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
                 if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+        }
+    };
+    if constexpr (Q <= 5) {
+        // r <= 2: rotate (Q copies of the plane body)
+        for (int l0 = 0; l0 < nload; l0 += Q)
+            static_for<0, Q>([&](auto ph) {
+                if (l0 + decltype(ph)::value < nload) plane(l0 + decltype(ph)::value, ph);
+            });
+    } else {
+        // r >= 3: the 7-9 body copies cost more in instruction cache than the
+        // 2r moves per point they save (measured: C3 order 8 379 -> 359 Gpts/s);
+        // shift the queue and keep phase 0
+        for (int l = 0; l < nload; ++l) {
+#pragma unroll
+            for (int i = 0; i < 2 * R; ++i)
+#pragma unroll
+                for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = q[i + 1][yy];
+            plane(l, std::integral_constant<int, 0>{});
         }
     }
 }
@@ -501,7 +533,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
 
     const int tx = tid % C::NTX, ty = tid / C::NTX;
     const int xb = x0 + 4 * tx;
-    const int64_t nx = prm.nx;
+    const int nx = (int)prm.nx;
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
@@ -535,8 +567,8 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
             const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
-            const int64_t gz = prm.gz0 + zt + yy;
-            const bool inz = (gz >= R) && (gz < prm.nzg - R);
+            const int gz = (int)prm.gz0 + zt + yy;
+            const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float pc = a[4 + e];
@@ -582,7 +614,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
                 }
             }
         }
-        if (xb < prm.pitch) {
+        if (xb < (int)prm.pitch) {
             float *dst = prm.pnext + (int64_t)(zt + R) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)

@@ -96,7 +96,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     // plane z1 = z0 - r + a.  Stage A iteration a (l = a + 2r) computes P^{k+1}(z1);
     // stage B iteration a (a >= 2r) computes P^{k+2}(z2 = z1 - r).
     const int nload = (z1e - z0) + 4 * R, na = nload - 2 * R;
-    const int64_t nx = prm.nx, ny = prm.ny;
+    const int nx = (int)prm.nx, ny = (int)prm.ny;   // 32-bit index math (dims <= 2^30)
     const int64_t kk = step_index(prm);
     constexpr float c0 = tap(R, 0);
     int rp = prm.rec.off ? prm.rec.off[unit] : 0;
@@ -173,8 +173,8 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             const int s1 = a % C::NS1;
             mbar_wait(&empty1[s1], ((a / C::NS1) & 1) ^ 1);
             float *t1 = sP1 + s1 * C::EF;
-            const int64_t gz = prm.gz0 + z1;
-            const bool inz = (gz >= R) && (gz < prm.nzg - R);
+            const int gz = (int)prm.gz0 + z1;
+            const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
             const bool store = (z1 >= z0) && (z1 < z1e);
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
 #pragma unroll
@@ -222,7 +222,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         }
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (store && interior && xb < prm.pitch)
+                    if (store && interior && xb < (int)prm.pitch)
                         *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + R) * ny + y) * prm.pitch + xb) = o;
                 }
             }
@@ -299,8 +299,8 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         const float *tpk = sP0 + sp * C::P0F;
         const int sab = b % C::NSA;                         // aux plane z2
         const float *tk = sAux + sab * 2 * C::EF + C::EF;
-        const int64_t gz = prm.gz0 + z2;
-        const bool inz = (gz >= R) && (gz < prm.nzg - R);
+        const int gz = (int)prm.gz0 + z2;
+        const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
         float4 out[C::NYB];
         if (act) {
             float4 col[C::NYB + 2 * R];
@@ -367,7 +367,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     }
             }
         }
-        if (xb < prm.pitch) {
+        if (xb < (int)prm.pitch) {
             float *dst = prm.pnext2 + ((int64_t)(z2 + R) * ny + y0 + ri0) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
@@ -432,7 +432,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     __syncthreads();
     if (b1 <= b0) return;
     const int nload = b1 - b0;
-    const int64_t nx = prm.nx;
+    const int nx = (int)prm.nx;
     const int64_t kk = step_index(prm);
     constexpr float c0 = tap(R, 0);
     int rp = prm.rec.off ? prm.rec.off[unit] : 0;
@@ -490,8 +490,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = lds128(tk + offe);
-                    const int64_t gz = prm.gz0 + z;
-                    const bool inz = (gz >= R) && (gz < prm.nzg - R);
+                    const int gz = (int)prm.gz0 + z;
+                    const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
                     float4 o;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -517,7 +517,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         }
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (interior && xb < prm.pitch)
+                    if (interior && xb < (int)prm.pitch)
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + R) * prm.pitch + xb) = o;
                 }
             }
@@ -567,8 +567,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
                 const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                 const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4), k4 = lds128(tk + offe);
-                const int64_t gz = prm.gz0 + zt + yy;
-                const bool inz = (gz >= R) && (gz < prm.nzg - R);
+                const int gz = (int)prm.gz0 + zt + yy;
+                const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const float pc = av[4 + e];
@@ -610,7 +610,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     }
             }
         }
-        if (xb < prm.pitch) {
+        if (xb < (int)prm.pitch) {
             float *dst = prm.pnext2 + (int64_t)(zt + R) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
