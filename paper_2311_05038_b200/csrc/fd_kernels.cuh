@@ -20,11 +20,11 @@
 // memory holds exactly the P that step k+1's add_source would produce.  This
 // is the same fp32 add on the same operands as in-place injection.
 //
-// Memory layout (HBM): each field buffer holds (nz_local + 2r) planes of
+// Memory layout (HBM): each field buffer holds (nz_local + 4r) planes of
 // ny rows of `pitch` floats (pitch = nx rounded up to 32 floats = 128 B); plane
-// z of the slab lives at buffer plane z + r; the r planes on each side are
-// zero (single GPU / global faces) or halo copies (slabs).  K has nz_local
-// planes with the same pitch.
+// z of the slab lives at buffer plane z + 2r (halo_planes); the 2r planes on
+// each side are zero (single GPU / global faces) or halo copies (slabs).  K
+// has nz_local planes with the same pitch, plus r halo planes on each side.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -47,6 +47,13 @@ __host__ __device__ constexpr float tap(int R, int m) {
 __host__ __device__ constexpr double tap_scale(int R) {
     return R == 1 ? 1.0 : R == 2 ? 12.0 : R == 3 ? 180.0 : 5040.0;
 }
+
+// Field buffers carry 2r halo planes on each side of the owned z range (local
+// plane z lives at buffer plane z + 2r): r for a single step, 2r for the
+// two-steps-per-launch kernel, whose first stage computes P^{k+1} on r planes
+// beyond the slab from P^k taps r further out.  K carries r halo planes
+// (K plane z at K-halo-buffer plane z + r; see fd_runtime.cu).
+__host__ __device__ constexpr int halo_planes(int R) { return 2 * R; }
 
 struct Receivers {
     const int32_t *off;   // CSR offsets per work unit [nunits + 1] (fused kernel)
@@ -279,7 +286,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 #pragma unroll
                 for (int pc = 0; pc < C::NPP; ++pc)
                     tma_load_3d(sP + s * C::P_FLOATS + pc * C::PPAD, &map_p, &fullP[s], x0 - 4 + pc * C::PBW,
-                                y0 - C::HY, j + R);
+                                y0 - C::HY, j + halo_planes(R));
                 if (l >= 2 * R) {
                     const int z = j - R, kl = l - 2 * R, ks = kl % C::NSK;
                     mbar_wait(&emptyK[ks], ((kl / C::NSK) & 1) ^ 1);
@@ -287,7 +294,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                     float *dst = sK + ks * C::K_FLOATS;
 #pragma unroll
                     for (int pc = 0; pc < C::NTP; ++pc) {
-                        tma_load_3d(dst + pc * C::TBW, &map_pp, &fullK[ks], x0 + pc * C::TBW, y0, z + R);
+                        tma_load_3d(dst + pc * C::TBW, &map_pp, &fullK[ks], x0 + pc * C::TBW, y0, z + halo_planes(R));
                         tma_load_3d(dst + C::T_FLOATS + pc * C::TBW, &map_k, &fullK[ks], x0 + pc * C::TBW, y0, z);
                     }
                 }
@@ -437,7 +444,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         }
         // store p_next in place of p_prev (float4; rows outside the grid skipped)
         if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext + ((int64_t)(z + R) * ny + yb) * prm.pitch + xb;
+            float *dst = prm.pnext + ((int64_t)(z + halo_planes(R)) * ny + yb) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
                 if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
@@ -523,8 +530,8 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
                 mbar_wait(&empty[s], ((l / C::NS) & 1) ^ 1);
                 mbar_expect_tx(&full[s], C::STAGE_BYTES);
                 float *st = smem + s * C::STAGE;
-                tma_load_3d(st, &map_p, &full[s], x0 - 4, 0, rb);   // buffer plane (rb - R) + R
-                tma_load_3d(st + C::P_FLOATS, &map_pp, &full[s], x0, 0, rb + R);
+                tma_load_3d(st, &map_p, &full[s], x0 - 4, 0, rb - R + halo_planes(R));   // rows rb - r ..
+                tma_load_3d(st + C::P_FLOATS, &map_pp, &full[s], x0, 0, rb + halo_planes(R));
                 tma_load_3d(st + C::P_FLOATS + C::T_FLOATS, &map_k, &full[s], x0, 0, rb);
             }
         }
@@ -615,7 +622,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             }
         }
         if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext + (int64_t)(zt + R) * prm.pitch + xb;
+            float *dst = prm.pnext + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
                 if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
@@ -637,7 +644,7 @@ __global__ void naive_step_kernel(const StepParams prm) {
         const int64_t z = prm.zlo + t / npl;
         const int64_t rem = t % npl;
         const int64_t y = rem / nx, x = rem % nx;
-        const int64_t i = ((z + R) * ny + y) * P + x;     // index in a field buffer
+        const int64_t i = ((z + halo_planes(R)) * ny + y) * P + x;     // index in a field buffer
         const float pc = prm.p[i];
         const int64_t gz = prm.gz0 + z;
         float S = 0.f;
@@ -685,7 +692,7 @@ __global__ void d2_axis_kernel(const StepParams prm, float *__restrict__ out) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
-        const int64_t i = ((z + R) * ny + y) * P + x;      // field buffer index
+        const int64_t i = ((z + halo_planes(R)) * ny + y) * P + x;      // field buffer index
         const int64_t s = AXIS == 0 ? 1 : (AXIS == 1 ? P : ny * P);
         const int64_t ia = AXIS == 0 ? x : (AXIS == 1 ? y : prm.gz0 + z);
         const int64_t na = AXIS == 0 ? nx : (AXIS == 1 ? ny : prm.nzg);
@@ -708,7 +715,7 @@ __global__ void time_update_kernel(const StepParams prm, const float *__restrict
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
         const int64_t ik = (z * ny + y) * P + x;
-        const int64_t i = ((z + R) * ny + y) * P + x;
+        const int64_t i = ((z + halo_planes(R)) * ny + y) * P + x;
         float S = pxx[ik];
         if (NDIM == 3) S = __fadd_rn(S, pyy[ik]);
         S = __fadd_rn(S, pzz[ik]);
@@ -721,7 +728,7 @@ template <int R>
 __global__ void gather_receivers_kernel(const StepParams prm) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= prm.nrec_local) return;
-    const int64_t i = ((int64_t)(prm.rec.z[j] + R) * prm.ny + prm.rec.y[j]) * prm.pitch + prm.rec.x[j];
+    const int64_t i = ((int64_t)(prm.rec.z[j] + halo_planes(R)) * prm.ny + prm.rec.y[j]) * prm.pitch + prm.rec.x[j];
     trace_row_of(prm, step_index(prm))[prm.rec.id[j]] = prm.pnext[i];
 }
 
@@ -751,7 +758,7 @@ __global__ void inject_kernel(float *field, const StepParams prm) {
     const float *wn = w_next_of(prm, step_index(prm));
     for (int s = 0; s < prm.nsrc; ++s) {
         if (prm.sz[s] < 0 || prm.sz[s] >= prm.nz) continue;
-        const int64_t i = ((int64_t)(prm.sz[s] + R) * prm.ny + prm.sy[s]) * prm.pitch + prm.sx[s];
+        const int64_t i = ((int64_t)(prm.sz[s] + halo_planes(R)) * prm.ny + prm.sy[s]) * prm.pitch + prm.sx[s];
         const float v = field[i];
         prm.src_raw[s] = v;
         field[i] = __fadd_rn(v, wn[s]);

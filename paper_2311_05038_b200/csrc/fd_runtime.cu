@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -264,18 +265,21 @@ struct Region {
     int nrec = 0;
 };
 
-// A z-slab [z0, z1) of the global grid with its own buffers (halo planes r on
-// each side).  One per context, except FD_OPT_VSLABS (several on one GPU).
+// A z-slab [z0, z1) of the global grid with its own buffers (field buffers:
+// halo_planes(r) = 2r planes on each side; K: r).  One per context, except
+// FD_OPT_VSLABS (several on one GPU).
 struct Slab {
     int64_t z0 = 0, z1 = 0, nz = 0;
     float *F[4] = {nullptr, nullptr, nullptr, nullptr};   // field buffers (F[2], F[3]: TB2 only)
-    float *K = nullptr;
+    float *Kh = nullptr;                        // K allocation: r halo planes on each side
+    float *K = nullptr;                         // = Kh + r planes (local plane 0)
     float *D[3] = {nullptr, nullptr, nullptr};   // Pxx, Pyy, Pzz (unfused decomposition only)
     float *d_src_raw = nullptr;
     CUtensorMap mHalo[4], mTile[4], mK;        // single-step kernel maps per field buffer
     CUtensorMap mP0[4], mPm[4], mKe;           // TB2 maps
-    std::vector<Region> regions;
-    Region tb2;                                 // the TB2 launch (own tiles -> own receiver CSR)
+    std::vector<Region> regions;                // single-step launches
+    std::vector<Region> tb2;                    // temporal-blocking launches (own receiver CSRs)
+    bool has_lo = false, has_hi = false;        // z-neighbours (rank or virtual slab)
 };
 
 struct fd_ctx {
@@ -285,6 +289,7 @@ struct fd_ctx {
     int64_t z0 = 0, z1 = 0;               // planes owned by this context
     int64_t pitch = 0;
     int rank = 0, nranks = 1, device = 0;
+    int H = 0;                            // field-buffer halo planes per side (halo_planes(R))
     bool poisoned = false;
     bool started = false;
     bool injected = false;                // w_k already injected into the CUR buffers
@@ -331,7 +336,7 @@ struct fd_ctx {
 };
 
 static inline int64_t plane_floats(const fd_ctx *c) { return c->nyg * c->pitch; }
-static inline int64_t buf_floats(const fd_ctx *c, const Slab &s) { return (s.nz + 2 * c->R) * plane_floats(c); }
+static inline int64_t buf_floats(const fd_ctx *c, const Slab &s) { return (s.nz + 2 * c->H) * plane_floats(c); }
 static inline float *cur_buf(const fd_ctx *c, const Slab &s) { return s.F[c->icur]; }
 static inline float *prev_buf(const fd_ctx *c, const Slab &s) { return s.F[c->iprev]; }
 
@@ -366,11 +371,10 @@ static fd_status partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_
 static void free_slab(Slab &s) {
     for (auto &d : s.D) { dev_free(d); d = nullptr; }
     for (auto &f : s.F) { dev_free(f); f = nullptr; }
-    dev_free(s.K); dev_free(s.d_src_raw);
-    s.K = s.d_src_raw = nullptr;
+    dev_free(s.Kh); dev_free(s.d_src_raw);
+    s.Kh = s.K = s.d_src_raw = nullptr;
     for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
-    dev_free(s.tb2.d_rec);
-    s.tb2.d_rec = nullptr;
+    for (auto &r : s.tb2) { dev_free(r.d_rec); r.d_rec = nullptr; }
 }
 
 static void drop_graphs(fd_ctx *c) {
@@ -400,18 +404,21 @@ static void destroy_all(fd_ctx *c) {
 }
 
 // Allocate a slab's buffers and upload its K: from host velocities v (the
-// slab's planes), or -- when v is NULL -- copied from device K planes kdev.
-static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdev = nullptr) {
+// slab's planes; K halos zero until exchanged), or -- when v is NULL -- copied
+// with its r halo planes from a device K-halo buffer kdevh (planes z - r ..).
+static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdevh = nullptr) {
     const size_t fbytes = (size_t)buf_floats(c, s) * 4;
-    const size_t kbytes = (size_t)(s.nz * plane_floats(c)) * 4;
+    const size_t kbytes = (size_t)((s.nz + 2 * c->R) * plane_floats(c)) * 4;
     s.F[0] = (float *)dev_alloc(fbytes);
     s.F[1] = (float *)dev_alloc(fbytes);
-    s.K = (float *)dev_alloc(kbytes);
+    s.Kh = (float *)dev_alloc(kbytes);
+    s.K = s.Kh ? s.Kh + c->R * plane_floats(c) : nullptr;
     s.d_src_raw = (float *)dev_alloc(kMaxSources * 4);
-    if (!s.F[0] || !s.F[1] || !s.K || !s.d_src_raw)
+    if (!s.F[0] || !s.F[1] || !s.Kh || !s.d_src_raw)
         return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
     c->dev_bytes += 2.0 * fbytes + kbytes;
     if (v) {
+        CUDA_TRY(c, cudaMemset(s.Kh, 0, kbytes));
         // upload v into the pitched K buffer, then K = fl32((v dt/h)^2/scale)
         // in fp64 on the device (bitwise the host formula, R#7)
         CUDA_TRY(c, cudaMemcpy2D(s.K, c->pitch * 4, v, c->nxg * 4, c->nxg * 4, c->nyg * s.nz,
@@ -421,7 +428,7 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kde
         velocity_to_K_kernel<<<blocks, 256>>>(s.K, rows, c->nxg, c->pitch, c->dt, c->h, scale_of(c->R));
         CUDA_TRY(c, cudaGetLastError());
     } else {
-        CUDA_TRY(c, cudaMemcpy(s.K, kdev, kbytes, cudaMemcpyDeviceToDevice));
+        CUDA_TRY(c, cudaMemcpy(s.Kh, kdevh, kbytes, cudaMemcpyDeviceToDevice));
     }
     CUDA_TRY(c, cudaMemset(s.F[0], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.F[1], 0, fbytes));
@@ -502,7 +509,7 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
         if (e != cudaSuccess) return fail(FD_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
     }
     fd_ctx *c = new fd_ctx();
-    c->ndim = ndim; c->order = order; c->R = R; c->h = h; c->dt = dt;
+    c->ndim = ndim; c->order = order; c->R = R; c->H = halo_planes(R); c->h = h; c->dt = dt;
     c->nxg = nxg; c->nyg = nyg; c->nzg = nzg; c->z0 = z0; c->z1 = z1;
     c->rank = rank; c->nranks = nranks;
     cudaGetDevice(&c->device);
@@ -613,7 +620,7 @@ static void choose_tile(fd_ctx *c, int64_t span) {
 
 static fd_status make_maps(fd_ctx *c, Slab &s) {
     const TileCfg &t = tile_table()[c->tile];
-    const int64_t planes = s.nz + 2 * c->R;
+    const int64_t planes = s.nz + 2 * c->H;
     // 3D: boxes (x, y) of one plane; 2D: boxes of pbz / tbz rows (nyg = 1)
     const int hy = c->ndim == 3 ? c->R : 0;
     const int pby = c->ndim == 3 ? t.ty + 2 * hy : 1, tby = c->ndim == 3 ? t.ty : 1;
@@ -700,15 +707,41 @@ static fd_status split_virtual(fd_ctx *c, int n) {
         int64_t a, b;
         partition(nz, n, q, &a, &b);
         s.z0 = c->z0 + a; s.z1 = c->z0 + b; s.nz = b - a;
-        st = build_slab(c, s, nullptr, o.K + a * pf);
+        st = build_slab(c, s, nullptr, o.Kh + a * pf);     // K planes a - r .. b + r
         if (st) break;
         const size_t bytes = (size_t)(s.nz * pf) * 4;
         for (int f = 0; f < 2; ++f)
-            CUDA_TRY(c, cudaMemcpy(s.F[f] + c->R * pf, o.F[f] + (c->R + a) * pf, bytes, cudaMemcpyDeviceToDevice));
+            CUDA_TRY(c, cudaMemcpy(s.F[f] + c->H * pf, o.F[f] + (c->H + a) * pf, bytes, cudaMemcpyDeviceToDevice));
     }
     free_slab(o);
     c->slabs.swap(ns);
     return st;
+}
+
+struct XBuf { int b, depth; };
+static fd_status exchange(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_t st);
+
+// The launches of one slab: [0, nz) -- or, with the overlapped schedule, the
+// boundary planes that feed the exchange ([0, bw) and [nz - bw, nz) where a
+// neighbour exists) first, then the interior.  bw = r for single steps, 2r
+// with temporal blocking (the neighbour reads 2r planes of P^{k+2}).
+static void split_regions(const fd_ctx *c, const Slab &s, bool overlap, int32_t bw, const TileCfg *t, int occ,
+                          std::vector<Region> &out) {
+    out.clear();
+    const int32_t nz = (int32_t)s.nz;
+    auto add = [&](int32_t lo, int32_t hi, bool boundary) {
+        if (hi <= lo) return;
+        Region g;
+        g.zlo = lo; g.zhi = hi; g.boundary = boundary;
+        g.zchunks = t ? chunks_for(c, *t, occ, hi - lo) : 1;
+        out.push_back(g);
+    };
+    if (!overlap) { add(0, nz, false); return; }
+    const int32_t lo_end = s.has_lo ? std::min(bw, nz) : 0;
+    const int32_t hi_beg = s.has_hi ? std::max(nz - bw, lo_end) : nz;
+    if (s.has_lo) add(0, lo_end, true);
+    if (s.has_hi) add(hi_beg, nz, true);
+    add(lo_end, hi_beg, false);
 }
 
 static fd_status prepare(fd_ctx *c) {
@@ -729,15 +762,23 @@ static fd_status prepare(fd_ctx *c) {
         const TileCfg &t = tile_table()[c->tile];
         CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
     }
+    if (c->opt_tsteps == 0) {
+        // auto: temporal blocking where it is faster (measured, order 2: 3D 513
+        // vs 422 Gpts/s on C3, 2D 439 vs 376 on C2) unless a single-step tile is pinned
+        c->opt_tsteps = (c->R == 1 && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
+    }
+    const bool multi = c->nranks > 1 || c->slabs.size() > 1;
     // overlapped schedule (boundary planes + exchange on the comm stream,
     // interior on the user stream): NCCL ranks, and virtual slabs, which run
-    // the identical schedule with device-copy halos
-    const bool overlap = (c->nranks > 1 || c->slabs.size() > 1) && c->opt_kernel == 0;
+    // the identical schedule with device-copy halos.  Single steps exchange r
+    // planes of P per face; temporal blocking 2r of P^{k+2} and r of P^{k+1}
+    // per two steps.
+    const bool overlap = multi && c->opt_kernel == 0;
     c->overlap = overlap;
     for (size_t q = 0; q < c->slabs.size(); ++q) {
         Slab &s = c->slabs[q];
-        const bool has_lo = c->nranks > 1 ? c->rank > 0 : q > 0;
-        const bool has_hi = c->nranks > 1 ? c->rank < c->nranks - 1 : q + 1 < c->slabs.size();
+        s.has_lo = c->nranks > 1 ? c->rank > 0 : q > 0;
+        s.has_hi = c->nranks > 1 ? c->rank < c->nranks - 1 : q + 1 < c->slabs.size();
         if (c->opt_kernel == 0) {
             st = make_maps(c, s);
             if (st) return st;
@@ -752,40 +793,18 @@ static fd_status prepare(fd_ctx *c) {
                 c->dev_bytes += (double)db;
             }
         }
-        s.regions.clear();
-        const int32_t nz = (int32_t)s.nz, R = c->R;
-        auto add = [&](int32_t lo, int32_t hi, bool boundary) {
-            if (hi <= lo) return;
-            Region g;
-            g.zlo = lo; g.zhi = hi; g.boundary = boundary;
-            g.zchunks = (c->opt_kernel != 0) ? 1 : chunks_for(c, tile_table()[c->tile], c->occ, hi - lo);
-            s.regions.push_back(g);
-        };
-        if (overlap) {
-            // boundary planes first (they feed the exchange), interior overlaps it
-            const int32_t lo_end = has_lo ? R : 0;
-            const int32_t hi_beg = has_hi ? nz - R : nz;
-            if (has_lo) add(0, R, true);
-            if (has_hi) add(nz - R, nz, true);
-            add(lo_end, hi_beg, false);
-        } else {
-            add(0, nz, false);
-        }
+        // single steps between temporal-blocking launches refresh 2r halo planes
+        const int32_t bw = c->opt_tsteps == 2 ? c->H : c->R;
+        split_regions(c, s, overlap, bw, c->opt_kernel != 0 ? nullptr : &tile_table()[c->tile], c->occ, s.regions);
         for (auto &g : s.regions) {
             st = upload_region_receivers(c, s, g, c->opt_kernel != 0 ? nullptr : &tile_table()[c->tile]);
             if (st) return st;
         }
     }
-    if (c->opt_tsteps == 0) {
-        // auto: temporal blocking where it is faster (measured, order 2: 3D 513
-        // vs 422 Gpts/s on C3, 2D 439 vs 376 on C2) unless a single-step tile is pinned
-        c->opt_tsteps = (c->R == 1 && c->slabs.size() == 1 && c->nranks == 1 && c->opt_kernel == 0 &&
-                         c->opt_tile < 0) ? 2 : 1;
-    }
     if (c->opt_tsteps == 2) {
-        // temporal blocking: 3D r <= 2 or 2D, one slab, fused path
-        if ((c->ndim == 3 && c->R > 2) || c->slabs.size() != 1 || c->nranks != 1 || c->opt_kernel != 0)
-            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs a single-slab context (3D: r <= 2) and the fused kernel");
+        // temporal blocking: 3D r <= 2 or 2D, fused path
+        if ((c->ndim == 3 && c->R > 2) || c->opt_kernel != 0)
+            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs the fused kernel (3D: r <= 2)");
         const auto &tb = tb2_table();
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
             if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
@@ -795,35 +814,37 @@ static fd_status prepare(fd_ctx *c) {
         if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
         const TileCfg &t = tb[c->tb2];
         CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
-        Slab &s = c->slabs[0];
-        const size_t fbytes = (size_t)buf_floats(c, s) * 4;
-        for (int b = 2; b < 4; ++b) {
-            s.F[b] = (float *)dev_alloc(fbytes);
-            if (!s.F[b]) return fail(FD_ERR_NOMEM, "temporal-blocking buffer allocation failed");
-            CUDA_TRY(c, cudaMemset(s.F[b], 0, fbytes));
-            c->dev_bytes += (double)fbytes;
-        }
         const TileCfg &ts = tile_table()[c->tile];
-        const int64_t planes = s.nz + 2 * c->R;
-        // 3D boxes (x, y rows, 1 plane); 2D boxes (x, 1, z rows)
-        const bool d3 = c->ndim == 3;
-        const int py = d3 ? t.pbz : 1, pz = d3 ? 1 : t.pbz, ey = d3 ? t.tbz : 1, ez = d3 ? 1 : t.tbz;
-        const int sy = d3 ? ts.ty + 2 * c->R : 1, sz = d3 ? 1 : ts.pbz, ty1 = d3 ? ts.ty : 1, tz1 = d3 ? 1 : ts.tbz;
-        bool ok = make_map(&s.mKe, s.K, c->nxg, c->nyg, s.nz, c->pitch, t.tbw, ey, ez);
-        for (int b = 0; b < 4 && ok; ++b)
-            ok = make_map(&s.mP0[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, py, pz) &&
-                 make_map(&s.mPm[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, ey, ez) &&
-                 make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.pbw, sy, sz) &&
-                 make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.tbw, ty1, tz1);
-        if (!ok) {
-            c->poisoned = true;
-            return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed (temporal blocking)");
+        for (auto &s : c->slabs) {
+            const size_t fbytes = (size_t)buf_floats(c, s) * 4;
+            for (int b = 2; b < 4; ++b) {
+                s.F[b] = (float *)dev_alloc(fbytes);
+                if (!s.F[b]) return fail(FD_ERR_NOMEM, "temporal-blocking buffer allocation failed");
+                CUDA_TRY(c, cudaMemset(s.F[b], 0, fbytes));
+                c->dev_bytes += (double)fbytes;
+            }
+            const int64_t planes = s.nz + 2 * c->H;
+            // 3D boxes (x, y rows, 1 plane); 2D boxes (x, 1, z rows).  K through
+            // its halo buffer: stage A reads K on the r planes beyond the slab.
+            const bool d3 = c->ndim == 3;
+            const int py = d3 ? t.pbz : 1, pz = d3 ? 1 : t.pbz, ey = d3 ? t.tbz : 1, ez = d3 ? 1 : t.tbz;
+            const int sy = d3 ? ts.ty + 2 * c->R : 1, sz = d3 ? 1 : ts.pbz, ty1 = d3 ? ts.ty : 1, tz1 = d3 ? 1 : ts.tbz;
+            bool ok = make_map(&s.mKe, s.Kh, c->nxg, c->nyg, s.nz + 2 * c->R, c->pitch, t.tbw, ey, ez);
+            for (int b = 0; b < 4 && ok; ++b)
+                ok = make_map(&s.mP0[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.pbw, py, pz) &&
+                     make_map(&s.mPm[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, t.tbw, ey, ez) &&
+                     make_map(&s.mHalo[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.pbw, sy, sz) &&
+                     make_map(&s.mTile[b], s.F[b], c->nxg, c->nyg, planes, c->pitch, ts.tbw, ty1, tz1);
+            if (!ok) {
+                c->poisoned = true;
+                return fail(FD_ERR_CUDA, "cuTensorMapEncodeTiled failed (temporal blocking)");
+            }
+            split_regions(c, s, overlap, c->H, &t, c->tb2occ, s.tb2);
+            for (auto &g : s.tb2) {
+                st = upload_region_receivers(c, s, g, &t);
+                if (st) return st;
+            }
         }
-        s.tb2.zlo = 0;
-        s.tb2.zhi = (int32_t)s.nz;
-        s.tb2.zchunks = chunks_for(c, t, c->tb2occ, s.nz);
-        st = upload_region_receivers(c, s, s.tb2, &t);
-        if (st) return st;
     }
     if (overlap) {
         int lo = 0, hi = 0;
@@ -838,6 +859,10 @@ static fd_status prepare(fd_ctx *c) {
             c->poisoned = true;
             return fail(FD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
         }
+        // K halos (static; read by the temporal-blocking kernel) once
+        st = exchange(c, {{-1, c->R}}, c->stream);
+        if (st) return st;
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
     return FD_OK;
 }
@@ -1036,26 +1061,33 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
-// Halo exchange of the field that becomes P (buffer `which_next`: true = the
-// p_next buffer of the step just launched, false = the current buffer).
-// Virtual slabs: device copies on the user stream.  Ranks: NCCL send/recv of
-// r planes per face on the comm stream (owned planes [0,r) and [nz-r,nz) live
-// at buffer planes [r,2r) and [nz,nz+r); halos at [0,r) and [nz+r,nz+2r)).
-static fd_status exchange(fd_ctx *c, bool next, cudaStream_t st) {
-    const int64_t pf = plane_floats(c), R = c->R;
-    const size_t cnt = (size_t)(R * pf);
+// Halo exchange of `depth` planes per face of field buffer b (b = -1: K).
+// Owned planes [0, nz) of a field buffer live at buffer planes [H, H + nz)
+// (H = halo_planes(r) = 2r; K: r); the lower halo receives the neighbour's
+// top `depth` owned planes at [H - depth, H), the upper halo its bottom ones at
+// [H + nz, H + nz + depth).  Virtual slabs: device copies on stream st.
+// Ranks: NCCL send/recv in one group (same issue order on both sides of a
+// face, so the messages of several buffers pair up).
+static fd_status exchange(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_t st) {
+    const int64_t pf = plane_floats(c);
+    auto base = [&](Slab &s, int b) { return b < 0 ? s.Kh : s.F[b]; };
+    auto hoff = [&](int b) -> int64_t { return b < 0 ? c->R : c->H; };
     if (c->nranks > 1) {
         Slab &s = c->slabs[0];
-        float *buf = next ? prev_buf(c, s) : cur_buf(c, s);
         NcclApi &n = nccl();
         ncclResult_t r = n.GroupStart();
-        if (c->rank > 0) {
-            if (!r) r = n.Send(buf + R * pf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
-            if (!r) r = n.Recv(buf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
-        }
-        if (c->rank < c->nranks - 1) {
-            if (!r) r = n.Send(buf + s.nz * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
-            if (!r) r = n.Recv(buf + (s.nz + R) * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
+        for (const XBuf &x : xs) {
+            float *buf = base(s, x.b);
+            const int64_t H = hoff(x.b), d = x.depth;
+            const size_t cnt = (size_t)(d * pf);
+            if (c->rank > 0) {
+                if (!r) r = n.Send(buf + H * pf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
+                if (!r) r = n.Recv(buf + (H - d) * pf, cnt, kNcclFloat32, c->rank - 1, c->comm, st);
+            }
+            if (c->rank < c->nranks - 1) {
+                if (!r) r = n.Send(buf + (H + s.nz - d) * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
+                if (!r) r = n.Recv(buf + (H + s.nz) * pf, cnt, kNcclFloat32, c->rank + 1, c->comm, st);
+            }
         }
         ncclResult_t r2 = n.GroupEnd();
         if (r || r2) {
@@ -1066,16 +1098,20 @@ static fd_status exchange(fd_ctx *c, bool next, cudaStream_t st) {
     }
     for (size_t q = 0; q < c->slabs.size(); ++q) {
         Slab &s = c->slabs[q];
-        float *buf = next ? prev_buf(c, s) : cur_buf(c, s);
-        if (q > 0) {
-            Slab &l = c->slabs[q - 1];
-            const float *lb = next ? prev_buf(c, l) : cur_buf(c, l);
-            CUDA_TRY(c, cudaMemcpyAsync(buf, lb + l.nz * pf, cnt * 4, cudaMemcpyDeviceToDevice, st));
-        }
-        if (q + 1 < c->slabs.size()) {
-            Slab &u = c->slabs[q + 1];
-            const float *ub = next ? prev_buf(c, u) : cur_buf(c, u);
-            CUDA_TRY(c, cudaMemcpyAsync(buf + (s.nz + R) * pf, ub + R * pf, cnt * 4, cudaMemcpyDeviceToDevice, st));
+        for (const XBuf &x : xs) {
+            float *buf = base(s, x.b);
+            const int64_t H = hoff(x.b), d = x.depth;
+            const size_t bytes = (size_t)(d * pf) * 4;
+            if (q > 0) {
+                Slab &l = c->slabs[q - 1];
+                CUDA_TRY(c, cudaMemcpyAsync(buf + (H - d) * pf, base(l, x.b) + (H + l.nz - d) * pf, bytes,
+                                            cudaMemcpyDeviceToDevice, st));
+            }
+            if (q + 1 < c->slabs.size()) {
+                Slab &u = c->slabs[q + 1];
+                CUDA_TRY(c, cudaMemcpyAsync(buf + (H + s.nz) * pf, base(u, x.b) + H * pf, bytes,
+                                            cudaMemcpyDeviceToDevice, st));
+            }
         }
     }
     return FD_OK;
@@ -1093,7 +1129,8 @@ static fd_status one_step(fd_ctx *c) {
         for (auto &sl : c->slabs)
             for (auto &g : sl.regions)
                 if (g.boundary) launch_region(c, sl, g, c->comm_stream);
-        tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, true, c->comm_stream); }, false);
+        const int d = c->opt_tsteps == 2 ? c->H : c->R;     // = the boundary regions' width
+        tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, {{c->iprev, d}}, c->comm_stream); }, false);
         if (s) return s;
         CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
         for (auto &sl : c->slabs)
@@ -1104,7 +1141,10 @@ static fd_status one_step(fd_ctx *c) {
         for (auto &sl : c->slabs)
             for (auto &g : sl.regions) launch_region(c, sl, g, c->stream);
         if (c->slabs.size() > 1 || c->nranks > 1) {
-            tracked(c, FD_K_HALO, c->stream, [&] { s = exchange(c, true, c->stream); }, false);
+            // the new P (a single step between temporal-blocking launches
+            // needs all 2r halo planes; the new P_prev keeps its valid ones)
+            const int d = c->opt_tsteps == 2 ? c->H : c->R;
+            tracked(c, FD_K_HALO, c->stream, [&] { s = exchange(c, {{c->iprev, d}}, c->stream); }, false);
             if (s) return s;
         }
     }
@@ -1114,15 +1154,15 @@ static fd_status one_step(fd_ctx *c) {
     return FD_OK;
 }
 
-// One temporal-blocking launch: steps k and k+1 (fd_tb2.cuh).  Reads the
-// (cur, prev) buffers, writes P^{k+1} and P^{k+2} into the two free ones.
-static fd_status two_steps(fd_ctx *c) {
-    Slab &s = c->slabs[0];
-    Region &g = s.tb2;
+// Temporal blocking: steps k and k+1 in one pass (fd_tb2.cuh) per slab region.
+// Reads the (cur, prev) buffers, writes P^{k+1} and P^{k+2} into the two free
+// ones.  Slabs: 2r halo planes of P^{k+2} (the next pass's P^k, whose taps
+// reach 2r beyond the slab) and r of P^{k+1} (read pointwise on the r planes
+// beyond the slab) come from the neighbours -- on the overlapped schedule the
+// 2r-plane boundary regions run first on the comm stream and feed the
+// exchange while the interior region runs on the user stream.
+static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream_t st) {
     const TileCfg &t = tb2_table()[c->tb2];
-    int f1 = -1, f2 = -1;
-    for (int b = 0; b < 4; ++b)
-        if (b != c->icur && b != c->iprev) (f1 < 0 ? f1 : f2) = b;
     StepParams p;
     fill_params(c, s, &g, p, c->k);
     p.p = cur_buf(c, s);
@@ -1134,7 +1174,32 @@ static fd_status two_steps(fd_ctx *c) {
     const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
-    tracked(c, FD_K_FUSED, c->stream, [&] { t.launch(grid, t.smem, c->stream, m0, mm, s.mKe, p); });
+    tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, m0, mm, s.mKe, p); });
+}
+
+static fd_status two_steps(fd_ctx *c) {
+    int f1 = -1, f2 = -1;
+    for (int b = 0; b < 4; ++b)
+        if (b != c->icur && b != c->iprev) (f1 < 0 ? f1 : f2) = b;
+    fd_status s = FD_OK;
+    if (c->overlap) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_step, c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.tb2)
+                if (g.boundary) launch_tb2(c, sl, g, f1, f2, c->comm_stream);
+        tracked(c, FD_K_HALO, c->comm_stream,
+                [&] { s = exchange(c, {{f2, c->H}, {f1, c->R}}, c->comm_stream); }, false);
+        if (s) return s;
+        CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.tb2)
+                if (!g.boundary) launch_tb2(c, sl, g, f1, f2, c->stream);
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+    } else {
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.tb2) launch_tb2(c, sl, g, f1, f2, c->stream);
+    }
     CUDA_TRY(c, cudaGetLastError());
     c->iprev = f1;
     c->icur = f2;
@@ -1156,12 +1221,12 @@ static fd_status advance_plain(fd_ctx *c, int64_t m) {
 // ------------------------------------------------------------ CUDA graphs
 // kGraphSteps consecutive steps captured once per starting buffer parity and
 // replayed (launch-bound small grids).  Kernels read k = *d_k + offset; the
-// graph ends by advancing d_k.  Not used with the two-stream overlap schedule
-// or while profiling.
+// graph ends by advancing d_k.  Not used across NCCL ranks or while profiling.
 constexpr int64_t kGraphSteps = 16;
 
 static bool graphs_usable(const fd_ctx *c) {
-    return c->opt_graph && !c->overlap && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream;
+    // virtual slabs: the two-stream schedule is captured too (event fork/join)
+    return c->opt_graph && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream;
 }
 
 // Capture kGraphSteps steps starting from the current buffer roles; the
@@ -1331,7 +1396,10 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
             if (p.nsrc > 0) dispatch_inject(c, c->stream, cur_buf(c, sl), p);
         }
         if (c->slabs.size() > 1 || c->nranks > 1) {
-            s = exchange(c, false, c->stream);
+            // halos of P (2r for temporal blocking) and, for temporal
+            // blocking, r of P_prev (fd_set_wavefield may have set it)
+            if (c->opt_tsteps == 2) s = exchange(c, {{c->icur, c->H}, {c->iprev, c->R}}, c->stream);
+            else s = exchange(c, {{c->icur, c->R}}, c->stream);
             if (s) return s;
         }
         c->injected = true;
@@ -1391,7 +1459,7 @@ fd_status fd_get_wavefield(fd_ctx *c, int which, float *host_out) {
     for (auto &sl : c->slabs) {
         const float *buf = which == FD_FIELD_CUR ? cur_buf(c, sl) : prev_buf(c, sl);
         float *dst = host_out + (sl.z0 - c->z0) * c->nyg * c->nxg;
-        CUDA_TRY(c, cudaMemcpy2D(dst, c->nxg * 4, buf + (int64_t)c->R * pf, c->pitch * 4, c->nxg * 4,
+        CUDA_TRY(c, cudaMemcpy2D(dst, c->nxg * 4, buf + (int64_t)c->H * pf, c->pitch * 4, c->nxg * 4,
                                  c->nyg * sl.nz, cudaMemcpyDeviceToHost));
         if (which == FD_FIELD_CUR && c->injected && !c->src.empty()) {
             // the CUR buffer already holds w_k (eager injection): restore the raw
@@ -1482,7 +1550,7 @@ fd_status fd_set_wavefield(fd_ctx *c, int which, const float *host_in) {
     const int64_t pf = plane_floats(c);
     for (auto &sl : c->slabs) {
         float *buf = which == FD_FIELD_CUR ? cur_buf(c, sl) : prev_buf(c, sl);
-        CUDA_TRY(c, cudaMemcpy2D(buf + (int64_t)c->R * pf, c->pitch * 4,
+        CUDA_TRY(c, cudaMemcpy2D(buf + (int64_t)c->H * pf, c->pitch * 4,
                                  host_in + (sl.z0 - c->z0) * c->nyg * c->nxg, c->nxg * 4, c->nxg * 4,
                                  c->nyg * sl.nz, cudaMemcpyHostToDevice));
     }
@@ -1579,12 +1647,14 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->kernel = 2;
     if (c->opt_tsteps == 2 && c->tb2 >= 0) {
         const TileCfg &t = tb2_table()[c->tb2];
-        const Region &g = c->slabs[0].tb2;
         o->tile_x = t.tx; o->tile_y = t.ty; o->rows_per_thread = t.ny;
         o->p_stages = 2 * t.r + 1 + t.dp; o->k_stages = t.r + 1 + t.dk;
         o->threads_per_cta = t.threads; o->smem_bytes = t.smem;
-        o->zchunks = g.zchunks;
-        o->ctas = (int)(ntiles_of(c, t) * g.zchunks);
+        int ctas = 0, zc = 0;
+        for (auto &sl : c->slabs)
+            for (auto &g : sl.tb2) { ctas += (int)(ntiles_of(c, t) * g.zchunks); zc = std::max(zc, g.zchunks); }
+        o->zchunks = zc;
+        o->ctas = ctas;
         return FD_OK;
     }
     if (!c->started) choose_tile(c, c->z1 - c->z0);

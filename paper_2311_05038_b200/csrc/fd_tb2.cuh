@@ -111,14 +111,14 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 const int j = z0 - 2 * R + l, s = l % C::NSP;
                 mbar_wait(&emptyP[s], ((l / C::NSP) & 1) ^ 1);
                 mbar_expect_tx(&fullP[s], C::P0_BYTES);
-                tma_load_3d(sP0 + s * C::P0F, &map_p0, &fullP[s], x0 - 8, y0 - 2 * R, j + R);
+                tma_load_3d(sP0 + s * C::P0F, &map_p0, &fullP[s], x0 - 8, y0 - 2 * R, j + halo_planes(R));
                 if (l >= 2 * R) {
                     const int a = l - 2 * R, z1 = j - R, sa = a % C::NSA;
                     mbar_wait(&emptyA[sa], ((a / C::NSA) & 1) ^ 1);
                     mbar_expect_tx(&fullA[sa], C::AUX_BYTES);
                     float *dst = sAux + sa * 2 * C::EF;
-                    tma_load_3d(dst, &map_pm, &fullA[sa], x0 - 4, y0 - R, z1 + R);
-                    tma_load_3d(dst + C::EF, &map_k, &fullA[sa], x0 - 4, y0 - R, z1);
+                    tma_load_3d(dst, &map_pm, &fullA[sa], x0 - 4, y0 - R, z1 + halo_planes(R));
+                    tma_load_3d(dst + C::EF, &map_k, &fullA[sa], x0 - 4, y0 - R, z1 + R);   // K halo buffer
                 }
             }
         }
@@ -223,7 +223,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
                     if (store && interior && xb < (int)prm.pitch)
-                        *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + R) * ny + y) * prm.pitch + xb) = o;
+                        *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + halo_planes(R)) * ny + y) * prm.pitch + xb) = o;
                 }
             }
             if (store && rz == z1) {                              // owners: tile-interior A threads
@@ -368,7 +368,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             }
         }
         if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext2 + ((int64_t)(z2 + R) * ny + y0 + ri0) * prm.pitch + xb;
+            float *dst = prm.pnext2 + ((int64_t)(z2 + halo_planes(R)) * ny + y0 + ri0) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
                 if (y0 + ri0 + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
@@ -446,9 +446,9 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
                 mbar_expect_tx(&fullS[s], C::STAGE_BYTES);
                 float *st = sSt + s * C::STAGE;
-                tma_load_3d(st, &map_p0, &fullS[s], x0 - 8, 0, rb - 2 * R + R);        // rows rb-2r.. (+r halo)
-                tma_load_3d(st + C::P0F, &map_pm, &fullS[s], x0 - 4, 0, rb - R + R);   // rows rb-r..
-                tma_load_3d(st + C::P0F + C::EF, &map_k, &fullS[s], x0 - 4, 0, rb - R);
+                tma_load_3d(st, &map_p0, &fullS[s], x0 - 8, 0, rb - 2 * R + halo_planes(R));        // rows rb-2r.. (+r halo)
+                tma_load_3d(st + C::P0F, &map_pm, &fullS[s], x0 - 4, 0, rb - R + halo_planes(R));   // rows rb-r..
+                tma_load_3d(st + C::P0F + C::EF, &map_k, &fullS[s], x0 - 4, 0, rb);   // K halo buffer: rows rb - r ..
             }
         }
         return;
@@ -518,7 +518,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
                     if (interior && xb < (int)prm.pitch)
-                        *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + R) * prm.pitch + xb) = o;
+                        *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + halo_planes(R)) * prm.pitch + xb) = o;
                 }
             }
             if (rp < rend && prm.rec.z[rp] < rb + C::TY)              // owners: block-interior A threads
@@ -611,7 +611,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             }
         }
         if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext2 + (int64_t)(zt + R) * prm.pitch + xb;
+            float *dst = prm.pnext2 + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
                 if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];

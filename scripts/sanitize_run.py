@@ -9,7 +9,7 @@
 Covers the fused 3D and 2D kernels (r = 1 and 4, ragged sizes, several
 z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
 naive and unfused reference paths, and the two-steps-per-launch kernels
-(3D and 2D).
+(3D and 2D, one slab and virtual slabs).
 """
 import os
 import sys
@@ -26,7 +26,8 @@ def main():
     cases = [((19, 21, 37), 2), ((23, 18, 41), 8), ((40, 75), 2), ((45, 70), 8)]
     for dims, order in cases:
         vel = rng.uniform(1500, 2500, dims).astype(np.float32)
-        tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3}] \
+        tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3},
+              {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_VSLABS: 3}] \
             if (len(dims) == 2 or order <= 4) else []
         for opts in [{}, {fd.FD_OPT_ZCHUNKS: 3}, {fd.FD_OPT_VSLABS: 2}, {fd.FD_OPT_KERNEL: 1},
                      {fd.FD_OPT_KERNEL: 3}, {fd.FD_OPT_GRAPH: 0}, {fd.FD_OPT_TSTEPS: 1}] + tb:

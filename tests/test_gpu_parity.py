@@ -447,6 +447,49 @@ def test_reserve_then_step_bitwise(fd):
             assert np.array_equal(a, b), ts
 
 
+@pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((41, 29, 66), 4), ((96, 300), 2), ((70, 140), 8)])
+@pytest.mark.parametrize("nslabs", [2, 3, 7])
+def test_temporal_blocking_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs):
+    """Two steps per launch on z-slabs (2r halo planes of P^{k+2}, r of
+    P^{k+1} exchanged per launch; K halos once): bitwise equal to one slab
+    with single steps, across odd step counts, graph replay, nonzero initial
+    fields (both halos exchanged before the first launch) and sources /
+    receivers within 2r of the slab faces."""
+    vel = _rand_vel(dims, seed=53)
+    h, dt = 10.0, 0.5e-3
+    r = order // 2
+    f1 = oracle.partition(dims[0], nslabs, 1)[0]              # first and last slab faces
+    f2 = oracle.partition(dims[0], nslabs, nslabs - 1)[0]
+    mid = tuple(d // 2 for d in dims[1:])
+    src = [((f1,) + mid, 25.0, 0.02, 1.0), ((f1 - r,) + tuple(d // 3 for d in dims[1:]), 15.0, 0.03, -0.4),
+           ((f2 - 1,) + mid, 10.0, 0.05, 0.7), ((f2 + 2 * r - 1,) + mid, 20.0, 0.025, 0.2)]
+    recs = [(f1 - 1,) + mid, (f1,) + mid, (f1 - 2 * r,) + mid, (f2 + r,) + mid, (dims[0] - 3,) + mid]
+    rng = np.random.default_rng(59)
+    P0 = rng.standard_normal(dims).astype(np.float32) * 1e-3
+    Pm1 = rng.standard_normal(dims).astype(np.float32) * 1e-3
+    seq = (1, 2, 33, 17, 38)
+
+    def run(options):
+        with fd.Simulation(vel, h, dt, order, options=options) as sim:
+            sim.set_wavefield(fd.FD_FIELD_CUR, P0)
+            sim.set_wavefield(fd.FD_FIELD_PREV, Pm1)
+            for s in src:
+                sim.add_source(*s)
+            sim.set_receivers(recs)
+            for n in seq:
+                sim.step(n)
+            return (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces(), sim.info())
+
+    ref = run({fd.FD_OPT_TSTEPS: 1})
+    for graph in (1, 0):
+        got = run({fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_VSLABS: nslabs, fd.FD_OPT_GRAPH: graph})
+        assert got[3]["steps_per_launch"] == 2
+        for a, b in zip(got[:3], ref[:3]):
+            assert np.array_equal(a, b), (nslabs, graph)
+    Po, Ppo, To = oracle.run(vel, h, dt, order, sum(seq), src, recs, P0=P0, Pm1=Pm1)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
 @pytest.mark.parametrize("dims,order", [((90, 300), 2), ((131, 200), 4), ((75, 260), 6), ((64, 129), 8)])
 def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     from paper_2311_05038_b200 import fd as fdm
