@@ -169,29 +169,40 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *   FD_OPT_VSLABS    n >= 1: split the grid into n z-slabs on this one GPU with
  *                    device-copy halo exchange (tests the slab logic)
  *   FD_OPT_PROFILE   1: bracket every launch with CUDA events (fd_get_kernel_times)
- *   FD_OPT_TSTEPS    0 (default) auto: 2 for order-2 single-slab contexts (2D or 3D)
- *                    without a pinned FD_OPT_TILE, else 1.  1: one step per launch.
+ *   FD_OPT_TSTEPS    0 (default) auto: 2 for order 2 (2D or 3D) without a pinned
+ *                    FD_OPT_TILE, else 1.  1: one step per launch.
  *                    2: temporal blocking -- one launch advances two steps (reads
  *                    p, p_prev, K once, writes both new fields: 10 B instead of
  *                    16 B per grid-point update); bitwise equal
- *                    to single steps.  2D any order, 3D order <= 4; single-slab contexts.
+ *                    to single steps.  2D any order, 3D order <= 4; on z-slabs
+ *                    (ranks, FD_OPT_VSLABS) 2r + r halo planes per two steps.
  *   FD_OPT_TB2TILE   index of the temporal-blocking tile configuration (-1 auto)
  *   FD_OPT_RESERVE   n >= 0: finish setup now -- allocate the step tables for n more
  *                    steps and capture the CUDA graphs the next fd_step calls will
  *                    replay -- so no allocation, synchronisation or capture happens
  *                    inside a later timed fd_step (marks the context started)
+ *   FD_OPT_RESIDENT  0 (default) auto: single-slab grids of <= 2^17 points with no
+ *                    pinned FD_OPT_TILE / FD_OPT_TSTEPS run each fd_step(n) call as
+ *                    ONE launch of one thread-block cluster that keeps p, p_prev
+ *                    and K in its shared memory for all n steps (halo planes pushed
+ *                    through DSMEM, one cluster barrier per step);
+ *                    bitwise equal to the other kernels.  1: off.  2: on
+ *                    (FD_ERR_STATE at the first fd_step if the grid does not fit)
+ *   FD_OPT_CLUSTER   cluster size of FD_OPT_RESIDENT (0 auto = the largest of
+ *                    16, 8, 4, 2 that fits; else 2, 4, 8 or 16)
  * FD_OPT_ASYNC, FD_OPT_PROFILE and FD_OPT_RESERVE may be set at any time; the others only before
  * the first fd_step.  Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
 enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
        FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7, FD_OPT_TSTEPS = 8,
-       FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10 };
+       FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10, FD_OPT_RESIDENT = 11, FD_OPT_CLUSTER = 12 };
 fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
 
 /* Device time per kernel kind accumulated while FD_OPT_PROFILE = 1 (ms and launch
  * counts, arrays of FD_K_COUNT).  Synchronises with the pending events.
  * FD_K_HALO times the halo exchange (copies / NCCL), not a kernel of ours. */
 enum { FD_K_FUSED = 0, FD_K_NAIVE = 1, FD_K_GATHER = 2, FD_K_INJECT = 3, FD_K_PXX = 4,
-       FD_K_PYY = 5, FD_K_PZZ = 6, FD_K_TIME = 7, FD_K_HALO = 8, FD_K_COUNT = 9 };
+       FD_K_PYY = 5, FD_K_PZZ = 6, FD_K_TIME = 7, FD_K_HALO = 8, FD_K_RESIDENT = 9,
+       FD_K_COUNT = 10 };
 fd_status fd_get_kernel_times(fd_ctx *ctx, double *ms, int64_t *launches);
 fd_status fd_reset_kernel_times(fd_ctx *ctx);
 
@@ -207,7 +218,9 @@ typedef struct {
     int ctas, threads_per_cta, smem_bytes, zchunks;
     int order;
     double device_bytes;       /* bytes of device memory held                           */
-    int steps_per_launch;      /* 2 with temporal blocking (FD_OPT_TSTEPS), else 1       */
+    int steps_per_launch;      /* 2 with temporal blocking (FD_OPT_TSTEPS), 0 when each  */
+                               /* fd_step call is one cluster launch (FD_OPT_RESIDENT), else 1 */
+    int cluster_ctas;          /* CTAs of the resident cluster (FD_OPT_RESIDENT), else 0 */
 } fd_info;
 fd_status fd_get_info(fd_ctx *ctx, fd_info *out);
 

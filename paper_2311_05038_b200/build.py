@@ -14,7 +14,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfd.so"
 SOURCES = [CSRC / "fd_runtime.cu"]
-DEPS = SOURCES + [CSRC / "fd_kernels.cuh", ROOT / "include" / "fd.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "fd.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,7 +42,9 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES), "-ldl"]
+    # FD_NVCC_EXTRA: extra nvcc flags for A/B experiments (e.g. -DFD_MBAR_SUSPEND_NS=0)
+    extra = os.environ.get("FD_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

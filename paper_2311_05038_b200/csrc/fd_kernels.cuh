@@ -122,7 +122,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Wait for the phase with the given parity to complete.  try_wait with a
+// suspend-time hint parks the waiting warp in the barrier unit instead of
+// re-issuing try_wait/branch in a loop (measured: the spin loop was ~30 % of
+// the issued instructions of the two-step kernel, profiles/ncu_r03).
+#ifndef FD_MBAR_SUSPEND_NS
+#define FD_MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if FD_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(FD_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -132,6 +150,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
                                             int z) {

@@ -20,6 +20,7 @@
 #include "../../include/fd.h"
 #include "fd_kernels.cuh"
 #include "fd_tb2.cuh"
+#include "fd_resident.cuh"
 
 using namespace fdk;
 
@@ -324,6 +325,11 @@ struct fd_ctx {
     int opt_tsteps = 0;                   // 0 auto, 1 single steps, 2 temporal blocking (two steps/launch)
     int opt_tb2tile = -1;
     int tb2 = -1, tb2occ = 0;             // chosen tb2_table() entry
+    // FD_OPT_RESIDENT: whole fd_step calls in one cluster launch (fd_resident.cuh)
+    int opt_resident = 0, opt_cluster = 0;   // 0 auto / 1 off / 2 on; forced cluster size
+    bool resident = false;
+    int res_nc = 0, res_npmax = 0, res_threads = 0, res_smem = 0;
+    int32_t *d_res_rec = nullptr;         // receivers sorted by CTA + offsets
     bool overlap = false;                 // boundary/interior split on two streams
     int tile = -1, occ = 0, nsm = 148;
     // FD_OPT_PROFILE: CUDA events around every launch, folded into per-kernel sums
@@ -389,7 +395,8 @@ static void destroy_all(fd_ctx *c) {
     dev_free(c->d_traces);
     dev_free(c->d_wtab);
     dev_free(c->d_k);
-    c->d_traces = nullptr; c->d_wtab = nullptr; c->d_k = nullptr;
+    dev_free(c->d_res_rec);
+    c->d_traces = nullptr; c->d_wtab = nullptr; c->d_k = nullptr; c->d_res_rec = nullptr;
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     c->own_stream = nullptr;
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
@@ -721,6 +728,88 @@ static fd_status split_virtual(fd_ctx *c, int n) {
 struct XBuf { int b, depth; };
 static fd_status exchange(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_t st);
 
+// ------------------------------------------------------------ cluster-resident runs
+// Auto threshold: grids up to this many points run whole fd_step calls in one
+// cluster launch (launch-bound sizes).
+constexpr int64_t kResidentAutoPoints = (int64_t)1 << 17;
+
+static const void *resident_fn(int R, int ndim) {
+    switch (R * 10 + ndim) {
+    case 12: return (const void *)resident_kernel<1, 2>;
+    case 13: return (const void *)resident_kernel<1, 3>;
+    case 22: return (const void *)resident_kernel<2, 2>;
+    case 23: return (const void *)resident_kernel<2, 3>;
+    case 32: return (const void *)resident_kernel<3, 2>;
+    case 33: return (const void *)resident_kernel<3, 3>;
+    case 42: return (const void *)resident_kernel<4, 2>;
+    default: return (const void *)resident_kernel<4, 3>;
+    }
+}
+
+// Largest cluster (16, 8, 4, 2 CTAs, or the forced size) whose CTAs hold
+// their planes of p, p_prev (each with r halo planes per side) and K in
+// shared memory, own >= r planes each and can be co-scheduled.
+static bool resident_config(fd_ctx *c) {
+    if (c->nranks != 1 || c->slabs.size() != 1) return false;
+    const int64_t nz = c->nzg, PS = c->nyg * c->nxg;
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const void *fn = resident_fn(c->R, c->ndim);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const int cands[4] = {16, 8, 4, 2};
+    for (int nc : cands) {
+        if (c->opt_cluster > 0 && nc != c->opt_cluster) continue;
+        if (nz / nc < c->R || nz / nc < 1) continue;
+        const int64_t npmax = (nz + nc - 1) / nc;
+        const int64_t smem = (2 * (npmax + 2 * c->R) + npmax) * PS * 4;
+        if (smem > maxsm) continue;
+        const int64_t work = (nz / nc) * PS;
+        const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(32, (work + 31) / 32 * 32));
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = nc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(nc); cfg.blockDim = dim3(threads); cfg.dynamicSmemBytes = (size_t)smem;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        c->res_nc = nc; c->res_npmax = (int)npmax; c->res_threads = threads; c->res_smem = (int)smem;
+        return true;
+    }
+    return false;
+}
+
+// Receivers sorted by owning CTA (plane split of resident_kernel) + offsets.
+static fd_status upload_resident_receivers(fd_ctx *c) {
+    const int nc = c->res_nc, n = (int)c->rec.size();
+    const int64_t nz = c->nzg;
+    std::vector<std::pair<int, int>> ord;          // (cta, receiver)
+    for (int j = 0; j < n; ++j) {
+        int cta = 0;
+        while (cta + 1 < nc && nz * (cta + 1) / nc <= c->rec[j].g[0]) ++cta;
+        ord.push_back({cta, j});
+    }
+    std::stable_sort(ord.begin(), ord.end());
+    std::vector<int32_t> h((size_t)4 * n + nc + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        const RecDef &r = c->rec[ord[i].second];
+        h[i] = (int32_t)r.g[0]; h[n + i] = (int32_t)r.g[1]; h[2 * n + i] = (int32_t)r.g[2];
+        h[3 * n + i] = ord[i].second;
+    }
+    for (int q = 0, i = 0; q <= nc; ++q) {
+        while (i < n && ord[i].first < q) ++i;
+        h[4 * n + q] = i;
+    }
+    c->d_res_rec = (int32_t *)dev_alloc(h.size() * 4);
+    if (!c->d_res_rec) return fail(FD_ERR_NOMEM, "receiver table allocation failed");
+    CUDA_TRY(c, cudaMemcpy(c->d_res_rec, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    return FD_OK;
+}
+
 // The launches of one slab: [0, nz) -- or, with the overlapped schedule, the
 // boundary planes that feed the exchange ([0, bw) and [nz - bw, nz) where a
 // neighbour exists) first, then the interior.  bw = r for single steps, 2r
@@ -754,6 +843,24 @@ static fd_status prepare(fd_ctx *c) {
     }
     c->d_k = (int64_t *)dev_alloc(sizeof(int64_t));
     if (!c->d_k) return fail(FD_ERR_NOMEM, "step counter allocation failed");
+    if (c->opt_resident != 1 && c->opt_kernel == 0) {
+        // auto: small single-slab grids with no pinned tile / step mode
+        const bool want = c->opt_resident == 2 ||
+                          (c->nxg * c->nyg * c->nzg <= kResidentAutoPoints && c->opt_tile < 0 &&
+                           c->opt_tsteps == 0 && c->opt_vslabs == 1 && c->nranks == 1);
+        if (want) {
+            c->resident = resident_config(c);
+            if (!c->resident && c->opt_resident == 2)
+                return fail(FD_ERR_STATE, "FD_OPT_RESIDENT=2: the grid does not fit one cluster's shared memory "
+                                          "(single-slab contexts, >= r planes per CTA)");
+            if (c->resident) {
+                c->opt_tsteps = 1;
+                return upload_resident_receivers(c);
+            }
+        }
+    } else if (c->opt_resident == 2) {
+        return fail(FD_ERR_STATE, "FD_OPT_RESIDENT=2 needs the fused path (FD_OPT_KERNEL 0 or 2)");
+    }
     int64_t maxnz = 0;
     for (auto &s : c->slabs) maxnz = std::max(maxnz, s.nz);
     if (c->opt_kernel == 0) {
@@ -1117,6 +1224,36 @@ static fd_status exchange(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_
     return FD_OK;
 }
 
+// n steps in one cluster launch; the roles swap when n is odd.
+static fd_status resident_steps(fd_ctx *c, int64_t n) {
+    Slab &s = c->slabs[0];
+    while (n > 0) {
+        const int32_t m = (int32_t)std::min<int64_t>(n, (int64_t)1 << 30);
+        StepParams p;
+        fill_params(c, s, nullptr, p, c->k);
+        p.K = s.K;
+        const int nic = (m & 1) ? c->iprev : c->icur, nip = (m & 1) ? c->icur : c->iprev;
+        ResidentArgs ra{cur_buf(c, s), prev_buf(c, s), s.F[nic], s.F[nip], m, c->res_npmax, c->d_res_rec,
+                        (int32_t)c->rec.size()};
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c->res_nc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(c->res_nc); cfg.blockDim = dim3(c->res_threads);
+        cfg.dynamicSmemBytes = (size_t)c->res_smem; cfg.stream = c->stream;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        cudaError_t e = cudaSuccess;
+        void *args[2] = {(void *)&p, (void *)&ra};
+        tracked(c, FD_K_RESIDENT, c->stream,
+                [&] { e = cudaLaunchKernelExC(&cfg, resident_fn(c->R, c->ndim), args); });
+        CUDA_TRY(c, e);
+        c->icur = nic; c->iprev = nip;
+        c->k += m;
+        n -= m;
+    }
+    return FD_OK;
+}
+
 static fd_status one_step(fd_ctx *c) {
     fd_status s;
     if (c->overlap) {
@@ -1226,7 +1363,7 @@ constexpr int64_t kGraphSteps = 16;
 
 static bool graphs_usable(const fd_ctx *c) {
     // virtual slabs: the two-stream schedule is captured too (event fork/join)
-    return c->opt_graph && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream;
+    return c->opt_graph && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream && !c->resident;
 }
 
 // Capture kGraphSteps steps starting from the current buffer roles; the
@@ -1405,7 +1542,12 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         c->injected = true;
     }
     int64_t i = 0;
-    if (graphs_usable(c) && n >= kGraphSteps) {
+    if (c->resident) {
+        s = resident_steps(c, n);
+        if (s) return s;
+        i = n;
+    }
+    if (graphs_usable(c) && n - i >= kGraphSteps) {
         // replay G-step graphs; the device counter d_k carries k
         set_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, c->k);
         ++c->launches;
@@ -1600,6 +1742,14 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         c->opt_tb2tile = (int)v;
         return FD_OK;
     case FD_OPT_GRAPH: c->opt_graph = v ? 1 : 0; return FD_OK;
+    case FD_OPT_RESIDENT:
+        if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_RESIDENT must be 0, 1 or 2");
+        c->opt_resident = (int)v;
+        return FD_OK;
+    case FD_OPT_CLUSTER:
+        if (v != 0 && v != 2 && v != 4 && v != 8 && v != 16) return fail(FD_ERR_ARG, "FD_OPT_CLUSTER must be 0, 2, 4, 8 or 16");
+        c->opt_cluster = (int)v;
+        return FD_OK;
     case FD_OPT_VSLABS:
         if (v < 1 || v > 64) return fail(FD_ERR_ARG, "FD_OPT_VSLABS must be in [1, 64]");
         if (c->nranks > 1 && v != 1) return fail(FD_ERR_ARG, "FD_OPT_VSLABS is for single-process contexts");
@@ -1645,6 +1795,12 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->steps_per_launch = (c->opt_tsteps == 2) ? 2 : 1;
     if (c->opt_kernel != 0) { o->kernel = c->opt_kernel; return FD_OK; }
     o->kernel = 2;
+    if (c->resident) {
+        o->steps_per_launch = 0;
+        o->cluster_ctas = c->res_nc;
+        o->ctas = c->res_nc; o->threads_per_cta = c->res_threads; o->smem_bytes = c->res_smem;
+        return FD_OK;
+    }
     if (c->opt_tsteps == 2 && c->tb2 >= 0) {
         const TileCfg &t = tb2_table()[c->tb2];
         o->tile_x = t.tx; o->tile_y = t.ty; o->rows_per_thread = t.ny;

@@ -8,8 +8,8 @@
 
 Covers the fused 3D and 2D kernels (r = 1 and 4, ragged sizes, several
 z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
-naive and unfused reference paths, and the two-steps-per-launch kernels
-(3D and 2D, one slab and virtual slabs).
+naive and unfused reference paths, the two-steps-per-launch kernels
+(3D and 2D, one slab and virtual slabs) and the cluster-resident kernel.
 """
 import os
 import sys
@@ -31,6 +31,9 @@ def main():
             if (len(dims) == 2 or order <= 4) else []
         for opts in [{}, {fd.FD_OPT_ZCHUNKS: 3}, {fd.FD_OPT_VSLABS: 2}, {fd.FD_OPT_KERNEL: 1},
                      {fd.FD_OPT_KERNEL: 3}, {fd.FD_OPT_GRAPH: 0}, {fd.FD_OPT_TSTEPS: 1}] + tb:
+            # these small grids would take the cluster-resident path by default:
+            # off here, on in its own case below
+            opts = {fd.FD_OPT_RESIDENT: 1, **opts}
             with fd.Simulation(vel, 10.0, 5e-4, order, options=opts) as sim:
                 sim.add_source(tuple(d // 2 for d in dims), 25.0, 0.02)
                 sim.set_receivers([tuple(d // 3 for d in dims), tuple(d - 1 for d in dims)])
@@ -39,6 +42,16 @@ def main():
                 T = sim.traces()
                 assert np.all(np.isfinite(P)) and np.all(np.isfinite(T))
             print("ok", dims, order, opts, flush=True)
+        # whole fd_step calls in one cluster launch (DSMEM halo pushes)
+        for ncl in (0, 4):
+            with fd.Simulation(vel, 10.0, 5e-4, order,
+                               options={fd.FD_OPT_RESIDENT: 2, fd.FD_OPT_CLUSTER: ncl}) as sim:
+                sim.add_source(tuple(d // 2 for d in dims), 25.0, 0.02)
+                sim.set_receivers([tuple(d // 3 for d in dims), tuple(d - 1 for d in dims)])
+                sim.step(7)
+                sim.step(13)
+                assert np.all(np.isfinite(sim.wavefield())) and np.all(np.isfinite(sim.traces()))
+            print("ok", dims, order, "resident", ncl, flush=True)
 
 
 if __name__ == "__main__":

@@ -43,8 +43,17 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / nb)
 
 
+def tiled(fd, options=None):
+    """Options with the cluster-resident path off (FD_OPT_RESIDENT=1) unless
+    set: the small grids of these tests would otherwise run whole fd_step
+    calls as one cluster launch (its own tests are test_resident_*)."""
+    o = {fd.FD_OPT_RESIDENT: 1}
+    o.update(options or {})
+    return o
+
+
 def run_gpu(fd, vel, h, dt, order, steps, sources, receivers, options=None, P0=None, Pm1=None):
-    with fd.Simulation(vel, h, dt, order, options=options) as sim:
+    with fd.Simulation(vel, h, dt, order, options=tiled(fd, options)) as sim:
         if P0 is not None:
             sim.set_wavefield(fd.FD_FIELD_CUR, P0)
         if Pm1 is not None:
@@ -131,7 +140,8 @@ def test_fused_equals_naive_bitwise_all_tiles(fd, dims, order):
 # Bit-exact contracts: indexing, band, traces, symmetry, light cone
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("ndim,order", [(2, 2), (2, 8), (3, 2), (3, 4), (3, 8)])
-def test_light_cone_mask_matches_oracle(fd, oracle, ndim, order):
+@pytest.mark.parametrize("resident", [1, 2])
+def test_light_cone_mask_matches_oracle(fd, oracle, ndim, order, resident):
     """After j steps from a point source, the nonzero mask of the fp32 field is
     the oracle's (equal for j <= 8): any misplaced tap, index or halo plane
     creates a nonzero outside it."""
@@ -141,7 +151,7 @@ def test_light_cone_mask_matches_oracle(fd, oracle, ndim, order):
     s = tuple([n // 2 - 2] + [n // 2 + 1] * (ndim - 1))
     src = [(s, 25.0, 0.0, 1.0)]
     for j in (1, 2, 5, 8):
-        P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, j, src, [])
+        P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, j, src, [], options={fd.FD_OPT_RESIDENT: resident})
         Po, Ppo, _ = oracle.run(vel, 10.0, 1e-3, order, j, src)
         assert np.array_equal(P != 0, Po != 0), j
         assert np.array_equal(Pp != 0, Ppo != 0), j
@@ -169,7 +179,7 @@ def test_incremental_steps_equal_one_call(fd):
     src = [((13, 20, 45), 25.0, 0.02, 1.0)]
     recs = [(13, 20, 50)]
     P1, Pp1, T1, _ = run_gpu(fd, vel, 10.0, 1e-3, 8, 30, src, recs)
-    with fd.Simulation(vel, 10.0, 1e-3, 8) as sim:
+    with fd.Simulation(vel, 10.0, 1e-3, 8, options=tiled(fd)) as sim:
         sim.add_source(*src[0])
         sim.set_receivers(recs)
         for n in (1, 0, 7, 22):
@@ -179,12 +189,14 @@ def test_incremental_steps_equal_one_call(fd):
 
 
 @pytest.mark.parametrize("ndim,order", [(2, 2), (2, 8), (3, 2), (3, 8)])
-def test_band_exactly_zero_and_mirror_symmetry(fd, ndim, order):
+@pytest.mark.parametrize("resident", [1, 2])
+def test_band_exactly_zero_and_mirror_symmetry(fd, ndim, order, resident):
     n = 65 if ndim == 2 else 33
     dims = (n,) * ndim
     vel = np.full(dims, 2000.0, np.float32)
     c = tuple([n // 2] * ndim)
-    P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, 60, [(c, 25.0, 0.04, 1.0)], [])
+    P, Pp, _, _ = run_gpu(fd, vel, 10.0, 1e-3, order, 60, [(c, 25.0, 0.04, 1.0)], [],
+                          options={fd.FD_OPT_RESIDENT: resident})
     r = order // 2
     for X in (P, Pp):
         for ax in range(ndim):
@@ -346,7 +358,7 @@ def test_unfused_decomposition_equals_fused(fd, dims, order):
 def test_profile_counts_fused_launches(fd):
     dims = (40, 40, 64)
     vel = _rand_vel(dims, seed=29)
-    with fd.Simulation(vel, 10.0, 1e-3, 4) as sim:
+    with fd.Simulation(vel, 10.0, 1e-3, 4, options=tiled(fd)) as sim:
         sim.add_source((20, 20, 32), 25.0, 0.02)
         sim.step(3)
         fd.fd_set_option(sim.ctx, fd.FD_OPT_PROFILE, 1)
@@ -367,7 +379,8 @@ def test_cuda_graph_replay_bitwise(fd, dims, kernel):
     recs = [tuple(d // 2 + 1 for d in dims), tuple(d // 4 for d in dims)]
     outs = []
     for graph in (0, 1):
-        with fd.Simulation(vel, 10.0, 1e-3, 4, options={fd.FD_OPT_GRAPH: graph, fd.FD_OPT_KERNEL: kernel}) as sim:
+        with fd.Simulation(vel, 10.0, 1e-3, 4,
+                           options=tiled(fd, {fd.FD_OPT_GRAPH: graph, fd.FD_OPT_KERNEL: kernel})) as sim:
             for s in src:
                 sim.add_source(*s)
             sim.set_receivers(recs)
@@ -516,6 +529,98 @@ def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     assert ntb >= 2
     Po, _, To = oracle.run(vel, h, dt, order, 41, src, recs)
     assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# Cluster-resident runs (FD_OPT_RESIDENT): one launch per fd_step call, the
+# fields in the cluster's shared memory, halos pushed through DSMEM
+# ---------------------------------------------------------------------------
+RES_CASES = [((256, 256), 2), ((256, 256), 8), ((90, 300), 4), ((61, 600), 6), ((37, 45, 70), 2),
+             ((29, 24, 30), 6), ((40, 20, 24), 8), ((33, 17, 19), 4)]
+
+
+@pytest.mark.parametrize("dims,order", RES_CASES)
+def test_resident_cluster_bitwise(fd, oracle, dims, order):
+    """Bitwise equal to the tiled kernels for every cluster size that fits,
+    across fd_step calls of odd lengths (roles swap inside the launch), with
+    nonzero initial fields, sources on CTA plane boundaries (pushed halo
+    copies), two sources on one point (registration order), a source in the
+    band and receivers at a source, on boundary planes and in the band."""
+    vel = _rand_vel(dims, seed=61)
+    h, dt = 10.0, 0.5e-3
+    r = order // 2
+    nz = dims[0]
+    rest = tuple(d // 2 for d in dims[1:])
+    src = [((nz // 2,) + rest, 25.0, 0.02, 1.0), ((nz // 2,) + rest, 12.0, 0.03, -0.5),
+           ((nz // 4,) + tuple(d // 3 for d in dims[1:]), 18.0, 0.025, 0.7),
+           ((r - 1,) + tuple(d // 4 for d in dims[1:]), 20.0, 0.02, 0.3)]
+    recs = [(nz // 2,) + rest, (nz // 2 - 1,) + rest, (nz // 4 + 1,) + rest, (0,) + rest,
+            (nz - 1 - r,) + tuple(d // 5 for d in dims[1:])]
+    rng = np.random.default_rng(67)
+    P0 = rng.standard_normal(dims).astype(np.float32) * 1e-3
+    Pm1 = rng.standard_normal(dims).astype(np.float32) * 1e-3
+    seq = (1, 0, 6, 17, 2, 21)
+
+    def run(options):
+        with fd.Simulation(vel, h, dt, order, options=options) as sim:
+            sim.set_wavefield(fd.FD_FIELD_CUR, P0)
+            sim.set_wavefield(fd.FD_FIELD_PREV, Pm1)
+            for s in src:
+                sim.add_source(*s)
+            sim.set_receivers(recs)
+            for n in seq:
+                sim.step(n)
+            return (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces(), sim.info())
+
+    ref = run({fd.FD_OPT_RESIDENT: 1, fd.FD_OPT_TSTEPS: 1})
+    sizes = []
+    for ncl in (2, 4, 8, 16):
+        try:
+            got = run({fd.FD_OPT_RESIDENT: 2, fd.FD_OPT_CLUSTER: ncl})
+        except fd.FDError as e:
+            assert e.status == fd.FD_ERR_STATE, e
+            continue
+        info = got[3]
+        assert info["steps_per_launch"] == 0 and info["cluster_ctas"] == ncl
+        assert info["kernel_launches"] <= 2 * len(seq)          # injection + one launch per call
+        sizes.append(ncl)
+        for a, b in zip(got[:3], ref[:3]):
+            assert np.array_equal(a, b), ncl
+    assert len(sizes) >= (2 if len(dims) == 2 else 1), sizes
+    Po, Ppo, To = oracle.run(vel, h, dt, order, sum(seq), src, recs, P0=P0, Pm1=Pm1)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[1], Ppo) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+def test_resident_auto_c1(fd, oracle):
+    """C1 (256 x 256, BASELINE configs[0]) takes the cluster path by default:
+    one launch per fd_step call; parity with the oracle."""
+    from workloads import config
+    wl = config("C1", order=2, steps=120)
+    vel = wl.vel()
+    with fd.Simulation(vel, wl.h, wl.dt, wl.order) as sim:
+        for s in wl.sources:
+            sim.add_source(s.idx, s.f, s.t0, s.amp)
+        sim.set_receivers(wl.receivers)
+        sim.step(wl.steps)
+        P, T, info = sim.wavefield(), sim.traces(), sim.info()
+    assert info["cluster_ctas"] >= 2 and info["steps_per_launch"] == 0
+    assert info["kernel_launches"] == 2                          # initial injection + the run
+    src = [(s.idx, s.f, s.t0, s.amp) for s in wl.sources]
+    Po, _, To = oracle.run(vel, wl.h, wl.dt, wl.order, wl.steps, src, wl.receivers, nthreads=4)
+    assert rel_l2(P, Po) <= TOL and rel_l2(T, To) <= TOL
+
+
+def test_resident_refuses_what_does_not_fit(fd):
+    vel = _rand_vel((64, 64, 64), seed=71)           # 3 MB of fields: more than 16 x 227 KB
+    with pytest.raises(fd.FDError) as e:
+        with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_RESIDENT: 2}) as sim:
+            sim.step(1)
+    assert e.value.status == fd.FD_ERR_STATE
+    with pytest.raises(fd.FDError) as e:
+        with fd.Simulation(vel[:20, :20, :20].copy(), 10.0, 1e-3, 2,
+                           options={fd.FD_OPT_RESIDENT: 2, fd.FD_OPT_VSLABS: 2}) as sim:
+            sim.step(1)
+    assert e.value.status == fd.FD_ERR_STATE
 
 
 # ---------------------------------------------------------------------------
