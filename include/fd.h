@@ -169,8 +169,9 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *   FD_OPT_VSLABS    n >= 1: split the grid into n z-slabs on this one GPU with
  *                    device-copy halo exchange (tests the slab logic)
  *   FD_OPT_PROFILE   1: bracket every launch with CUDA events (fd_get_kernel_times)
- *   FD_OPT_TSTEPS    0 (default) auto: 2 for order 2 (2D or 3D) without a pinned
- *                    FD_OPT_TILE, else 1.  1: one step per launch.
+ *   FD_OPT_TSTEPS    0 (default) auto: 2 for 3D order 2 and 2D orders 2 and 4 (where
+ *                    it is faster) without a pinned FD_OPT_TILE, else 1.  1: one
+ *                    step per launch.
  *                    2: temporal blocking -- one launch advances two steps (reads
  *                    p, p_prev, K once, writes both new fields: 10 B instead of
  *                    16 B per grid-point update); bitwise equal

@@ -187,18 +187,27 @@ static TileCfg make_tb2d() {
 
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = {
-        // r01/r03 sweeps (C3, order 2): 504-516 / 444 / 425 / 418 Gpts/s; none of
-        // (64x8, 32x16, 128x8, deeper rings) beat the first
-        make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 64, 16, 3, 4, 2, 2, 2>(),
-        make_tb2ws<1, 64, 16, 2, 4, 1, 1, 1, 2>(), make_tb2ws<1, 64, 16, 2, 2, 2, 2, 2, 2>(),
-        make_tb2ws<1, 64, 16, 2, 4, 3, 3, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
+        // 3D r=1, r04 sweep (C3 order 2, scripts/tune.py --tsteps 2): one
+        // 128 x 16 CTA per SM with 6-slot P^k / 5-slot aux rings 581-584 Gpts/s;
+        // the r03 choice (64 x 16, two CTAs per SM, 5/4 slots) 518; 64 x 16 with
+        // 6/5 slots 542; 128 x 16 with 5/4 slots 534; more stage-B warps
+        // (NYB = 2) 481-551
+        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1>(),
+        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 3, 1>(), make_tb2ws<1, 64, 16, 2, 4, 3, 3, 1, 2>(),
+        make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
+        // 3D r=2 (order 4 stays on single steps by default: 421 vs <= 320 Gpts/s in r03)
         make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
-        // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows
-        // (r01 sweep, C2: order 2 439 Gpts/s vs 376 single-step; order 4 368; order 8 239 vs 347)
-        make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(), make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
+        make_tb2ws<2, 64, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<2, 128, 8, 2, 2, 3, 3, 2, 1>(),
+        make_tb2ws<2, 64, 16, 2, 4, 2, 2, 2, 1>(),
+        // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows.  r04 sweep
+        // (C2): order 2 554 Gpts/s (3 stages, two CTAs per SM; 518 with 2) vs
+        // 400 single-step; order 4 486 vs 397; order 6 391 vs 392; order 8 328 vs 385
+        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
+        make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
         make_tb2d<2, 64, 28, 4, 4, 3, 2>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
         make_tb2d<3, 64, 26, 4, 2, 3, 2>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
-        make_tb2d<4, 64, 24, 4, 4, 3, 2>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>()};
+        make_tb2d<4, 64, 24, 4, 4, 3, 2>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
+        make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>()};
     return t;
 }
 
@@ -870,9 +879,12 @@ static fd_status prepare(fd_ctx *c) {
         CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
     }
     if (c->opt_tsteps == 0) {
-        // auto: temporal blocking where it is faster (measured, order 2: 3D 513
-        // vs 422 Gpts/s on C3, 2D 439 vs 376 on C2) unless a single-step tile is pinned
-        c->opt_tsteps = (c->R == 1 && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
+        // auto: temporal blocking where it is faster (r04 sweeps: 3D order 2
+        // 582 vs 426 Gpts/s on C3 -- order 4 375 vs 421 stays single; 2D order 2
+        // 554 vs 400 and order 4 486 vs 397 on C2 -- orders 6/8 stay single)
+        // unless a single-step tile is pinned
+        const bool tb_wins = c->ndim == 3 ? c->R == 1 : c->R <= 2;
+        c->opt_tsteps = (tb_wins && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
     }
     const bool multi = c->nranks > 1 || c->slabs.size() > 1;
     // overlapped schedule (boundary planes + exchange on the comm stream,
