@@ -333,24 +333,30 @@ def run_ours(args, wl):
     vel_pin = torch.empty(vel.shape, dtype=torch.float32, pin_memory=True).numpy()
     vel_pin[...] = vel
     out_pin = torch.empty(vel.shape, dtype=torch.float32, pin_memory=True).numpy()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    s2 = _make_sim(wl, world, vel_pin, gdims)
-    s2.step(args.steps)
-    T2 = s2.traces()
-    W2 = s2.wavefield(out=out_pin)
-    e2e_s = time.perf_counter() - t0     # results are on the host: teardown is not part of the job
-    s2.close()
-    if world > 1:
-        from paper_2311_05038_b200 import dist as fdd
-        e2e_s = fdd.max_over_ranks(e2e_s)
+    # three complete runs; the reported time is their median (host-side
+    # effects -- page-cache state, CPU clocks -- vary run to run)
+    runs = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        s2 = _make_sim(wl, world, vel_pin, gdims)
+        s2.step(args.steps)
+        T2 = s2.traces()
+        W2 = s2.wavefield(out=out_pin)
+        e2e_s = time.perf_counter() - t0     # results are on the host: teardown is not part of the job
+        s2.close()
+        if world > 1:
+            from paper_2311_05038_b200 import dist as fdd
+            e2e_s = fdd.max_over_ranks(e2e_s)
+        runs.append(e2e_s)
+    e2e_s = sorted(runs)[1]
     h2d = vel_pin.nbytes + 8 * len(wl.receivers) * wl.ndim
     d2h = T2.nbytes + W2.nbytes
     e2e = {"value": wl.npts * args.steps * world / e2e_s / 1e9, "unit": "Gpts/s",
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-           "seconds": e2e_s, "pinned_host_buffers": True,
+           "seconds": e2e_s, "seconds_runs": runs, "pinned_host_buffers": True,
            "what": "fd_create (model upload) + fd_step(K) + fd_get_traces + fd_get_wavefield"}
     return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes)
 
