@@ -161,6 +161,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("FD_BENCH_SHARE_GPU") == "1":
+        local = 0        # test hook: every rank on cuda:0 (peer transport, gloo plumbing)
     return rank, world, local
 
 
@@ -249,17 +251,18 @@ def _velocity(wl, world):
     return velocity(wl.model, gdims, z0, z1), gdims
 
 
-def _make_sim(wl, world, vel, gdims, stream=None, options=None):
+def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl"):
     """This rank's simulation: the whole grid at N=1; at N>1 a z-slab of the
     weak-scaled grid (N copies of the workload's grid stacked along z,
-    slab-decomposed, halo exchange over NCCL inside libfd.so)."""
+    slab-decomposed, halo exchange inside libfd.so: NCCL send/recv, or the
+    step kernels' peer stores with --transport peer)."""
     import paper_2311_05038_b200 as fd
     if world == 1:
         sim = fd.Simulation(vel, wl.h, wl.dt, wl.order, stream=stream, options=options)
     else:
         from paper_2311_05038_b200 import dist as fdd
-        sim = fdd.create(vel, gdims, wl.h, wl.dt, wl.order, device=int(os.environ.get("LOCAL_RANK", "0")),
-                         stream=stream, options=options)
+        sim = fdd.create(vel, gdims, wl.h, wl.dt, wl.order, device=dist_env()[2], stream=stream,
+                         options=options, transport=transport)
     for s in wl.sources:
         sim.add_source(s.idx, s.f, s.t0, s.amp)
     sim.set_receivers(wl.receivers)
@@ -275,14 +278,17 @@ def run_ours(args, wl):
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("FD_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     vel, gdims = _velocity(wl, world)
     stream = torch.cuda.Stream(device=dev)
     opts = {fd.FD_OPT_ASYNC: 1}
     if args.no_graph:
         opts[fd.FD_OPT_GRAPH] = 0
     opts[fd.FD_OPT_TSTEPS] = args.tsteps
-    sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts)
+    sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport)
     sim.step(args.warmup)
     # setup for the timed steps (trace/wavelet tables for both passes, the CUDA
     # graphs to replay) happens here, outside the timed region
@@ -319,7 +325,7 @@ def run_ours(args, wl):
     finite = bool(np.all(np.isfinite(T)))
     sim.close()
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -341,7 +347,7 @@ def run_ours(args, wl):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        s2 = _make_sim(wl, world, vel_pin, gdims)
+        s2 = _make_sim(wl, world, vel_pin, gdims, transport=args.transport)
         s2.step(args.steps)
         T2 = s2.traces()
         W2 = s2.wavefield(out=out_pin)
@@ -402,7 +408,9 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
         "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
                    "dt": wl.dt, "h": wl.h, "receivers": len(wl.receivers), "sources": len(wl.sources),
                    "l2": "no flush: per-step working set %.2f GB >> 126 MB L2" % (12.0 * wl.npts / 1e9),
-                   "parallelism": f"z-slabs x{world} (NCCL halo exchange)" if world > 1 else "1 GPU",
+                   "parallelism": (f"z-slabs x{world} ({'in-kernel peer-store' if args.transport == 'peer' else 'NCCL'}"
+                                   f" halo exchange)") if world > 1 else "1 GPU",
+                   **({"shared_gpu": True} if os.environ.get("FD_BENCH_SHARE_GPU") == "1" else {}),
                    "global_grid": [wl.dims[0] * world] + list(wl.dims[1:]),
                    "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -428,6 +436,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="plain launches instead of CUDA-graph replay")
     ap.add_argument("--clock-sampler", default="nvml", choices=["nvml", "smi"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="halo transport at N>1: NCCL send/recv or in-kernel peer stores (CUDA IPC)")
     ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (library default), 1 one step per launch, 2 temporal blocking (10 B/update)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -78,7 +78,7 @@ typedef struct {
     int device;            /* CUDA device ordinal to use (-1: the current device)     */
     const void *nccl_id;   /* 128-byte ncclUniqueId from fd_nccl_get_unique_id on rank 0,
                               broadcast by the caller (e.g. torch.distributed); may be
-                              NULL when nranks == 1                                    */
+                              NULL when nranks == 1 or with FD_OPT_TRANSPORT = 1       */
     int vel_is_slab;       /* 0: vel holds the global model; 1: only this rank's planes
                               [z0, z1) of fd_partition                                 */
 } fd_dist;
@@ -96,6 +96,24 @@ fd_status fd_partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *z
 
 /* Writes a fresh 128-byte ncclUniqueId to out128.  FD_ERR_NCCL if NCCL is unavailable. */
 fd_status fd_nccl_get_unique_id(void *out128);
+
+/* Peer transport (FD_OPT_TRANSPORT = 1): the step kernels store
+ * their boundary planes straight into the z-neighbours' halo planes (CUDA IPC
+ * mappings over NVLink) and a flag in the neighbour's memory orders the steps;
+ * no NCCL.  Protocol, before the first fd_step:
+ *   fd_peer_export(ctx, blob, cap, &len)  -- allocates all four field buffers and
+ *       the flags, freezes the options and writes an opaque blob
+ *       (<= FD_PEER_BLOB_BYTES) of IPC handles of this rank's field buffers, K and
+ *       flags (sources / receivers / initial fields may still be set after it);
+ *   the caller exchanges the blobs (e.g. torch.distributed all_gather);
+ *   fd_peer_import(ctx, lo_blob, hi_blob) -- the blobs of rank - 1 and rank + 1
+ *       (NULL at the global faces); opens the mappings.
+ * Errors: FD_ERR_STATE (not a multi-rank context with FD_OPT_TRANSPORT = 1, after
+ * the first fd_step, custom allocator set, blob of another grid), FD_ERR_ARG (cap
+ * too small, missing blob), FD_ERR_CUDA (IPC failure). */
+enum { FD_PEER_BLOB_BYTES = 512 };
+fd_status fd_peer_export(fd_ctx *ctx, void *blob, size_t cap, size_t *len);
+fd_status fd_peer_import(fd_ctx *ctx, const void *lo_blob, const void *hi_blob);
 
 /* Register a point source (add_source; R#4, R#5): before the stencil of step k,
  * P[idx] += amp * R(k dt) with the Ricker wavelet R(t) = (1 - 2 pi^2 f^2 (t-t0)^2)
@@ -191,11 +209,17 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *                    (FD_ERR_STATE at the first fd_step if the grid does not fit)
  *   FD_OPT_CLUSTER   cluster size of FD_OPT_RESIDENT (0 auto = the largest of
  *                    16, 8, 4, 2 that fits; else 2, 4, 8 or 16)
+ *   FD_OPT_TRANSPORT halo transport on z-slabs: 0 (default) NCCL send/recv across
+ *                    ranks, device copies across virtual slabs; 1 peer: the
+ *                    boundary-plane launches store their planes into the
+ *                    neighbours' halos in the kernel epilogue (virtual slabs: no
+ *                    copies; ranks: fd_peer_export / fd_peer_import, flag sync)
  * FD_OPT_ASYNC, FD_OPT_PROFILE and FD_OPT_RESERVE may be set at any time; the others only before
  * the first fd_step.  Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
 enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
        FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7, FD_OPT_TSTEPS = 8,
-       FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10, FD_OPT_RESIDENT = 11, FD_OPT_CLUSTER = 12 };
+       FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10, FD_OPT_RESIDENT = 11, FD_OPT_CLUSTER = 12,
+       FD_OPT_TRANSPORT = 13 };
 fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
 
 /* Device time per kernel kind accumulated while FD_OPT_PROFILE = 1 (ms and launch

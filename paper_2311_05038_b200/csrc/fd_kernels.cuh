@@ -63,6 +63,17 @@ struct Receivers {
     const int32_t *id;    // column in the step-major trace row
 };
 
+// Transport "peer" (FD_OPT_TRANSPORT): a store of local
+// plane z of a field buffer also writes the neighbouring slab's halo copy of
+// that plane when z is one of its `push` boundary planes -- through NVLink
+// (CUDA IPC mapping) across ranks, plain device memory across virtual slabs.
+// Our plane z is the lower neighbour's buffer plane lo_z + z (lo_z = its
+// nz + 2r) and the upper neighbour's buffer plane z - nz + 2r.
+struct PeerPush {
+    float *lo, *hi;         // the neighbours' buffer of the same role, or null
+    int32_t lo_z, push;
+};
+
 struct StepParams {
     int64_t nx, ny, nz;     // local extents (nz = owned planes)
     int64_t pitch;          // floats per row
@@ -89,7 +100,17 @@ struct StepParams {
     int32_t nrec_local;     // receivers of this launch's list (naive gather)
     float *traces;          // step-major [k][nrec_total]
     int32_t nrec_total;
+    PeerPush peer1, peer2;  // in-kernel halo pushes of pnext / pnext2 (boundary launches)
 };
+
+// `off` = offset of the float4 within its plane (y * pitch + x), `plane` = ny * pitch
+template <int R>
+__device__ __forceinline__ void peer_store4(const PeerPush &pp, int z, int nz, int64_t plane, int64_t off,
+                                            const float4 &v) {
+    if (pp.lo && z < pp.push) *reinterpret_cast<float4 *>(pp.lo + (int64_t)(z + pp.lo_z) * plane + off) = v;
+    if (pp.hi && z >= nz - pp.push)
+        *reinterpret_cast<float4 *>(pp.hi + (int64_t)(z - nz + halo_planes(R)) * plane + off) = v;
+}
 
 __device__ __forceinline__ int64_t step_index(const StepParams &p) { return p.kdev ? *p.kdev + p.koff : p.k; }
 __device__ __forceinline__ float *trace_row_of(const StepParams &p, int64_t k) {
@@ -466,7 +487,11 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             float *dst = prm.pnext + ((int64_t)(z + halo_planes(R)) * ny + yb) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
-                if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if (yb + yy < ny) {
+                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                    peer_store4<R>(prm.peer1, z, (int)prm.nz, (int64_t)ny * prm.pitch,
+                                   (int64_t)(yb + yy) * prm.pitch + xb, out[yy]);
+                }
         }
     };
     if constexpr (Q <= 5) {
@@ -644,7 +669,10 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             float *dst = prm.pnext + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
-                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if (zt + yy < prm.zhi) {
+                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                    peer_store4<R>(prm.peer1, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
+                }
         }
     }
 }
@@ -767,6 +795,25 @@ __global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64
 
 // graph bookkeeping: the device step counter
 __global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
+
+// Peer transport flag sync (fd_runtime.cu peer_signal / peer_wait): the
+// neighbours' flags count completed halo exchanges.  The signal runs after the
+// pushing launches in stream order; the system-scope fence and release store
+// publish their peer stores before the count.
+__global__ void peer_signal_kernel(int64_t *lo, int64_t *hi, int64_t v) {
+    __threadfence_system();
+    if (lo) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(lo), "l"(v) : "memory");
+    if (hi) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(hi), "l"(v) : "memory");
+}
+__global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi, int64_t v) {
+    for (;;) {
+        int64_t a = v, b = v;
+        if (need_lo) asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(a) : "l"(flags) : "memory");
+        if (need_hi) asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(b) : "l"(flags + 1) : "memory");
+        if (a >= v && b >= v) break;
+        __nanosleep(200);
+    }
+}
 __global__ void advance_step_kernel(int64_t *kdev, int64_t n) { *kdev += n; }
 
 // add_source on a field buffer, registration order; records the raw values.

@@ -339,6 +339,19 @@ struct fd_ctx {
     bool resident = false;
     int res_nc = 0, res_npmax = 0, res_threads = 0, res_smem = 0;
     int32_t *d_res_rec = nullptr;         // receivers sorted by CTA + offsets
+    // FD_OPT_TRANSPORT = 1: in-kernel halo pushes (peer stores) instead of copies / NCCL
+    int opt_transport = 0;
+    struct Peer {
+        float *F[4] = {nullptr, nullptr, nullptr, nullptr};   // the neighbour's field buffers (IPC)
+        float *Kh = nullptr;
+        int64_t *flags = nullptr;          // the neighbour's flag array
+        int64_t nz = 0;
+        std::vector<void *> opened;        // IPC mappings to close
+    } plo, phi;
+    bool peer_imported = false;
+    bool frozen = false;                  // fd_peer_export done: options fixed
+    int64_t *d_flags = nullptr;           // [0]: written by rank - 1, [1]: by rank + 1 (exchange counts)
+    int64_t xcount = 0;                   // exchanges this rank has signalled
     bool overlap = false;                 // boundary/interior split on two streams
     int tile = -1, occ = 0, nsm = 148;
     // FD_OPT_PROFILE: CUDA events around every launch, folded into per-kernel sums
@@ -405,6 +418,11 @@ static void destroy_all(fd_ctx *c) {
     dev_free(c->d_wtab);
     dev_free(c->d_k);
     dev_free(c->d_res_rec);
+    for (auto *pr : {&c->plo, &c->phi})
+        for (void *m : pr->opened) cudaIpcCloseMemHandle(m);
+    c->plo.opened.clear(); c->phi.opened.clear();
+    if (c->d_flags) cudaFree(c->d_flags);
+    c->d_flags = nullptr;
     c->d_traces = nullptr; c->d_wtab = nullptr; c->d_k = nullptr; c->d_res_rec = nullptr;
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     c->own_stream = nullptr;
@@ -476,7 +494,6 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
         if (s) return s;
         if (nranks > 1 && z1 - z0 < 2 * R)
             return fail(FD_ERR_ARG, "slab of %lld planes thinner than 2r=%d", (long long)(z1 - z0), 2 * R);
-        if (nranks > 1 && !nccl_id) return fail(FD_ERR_ARG, "nccl_id is NULL with nranks > 1");
     }
     const int64_t nz = z1 - z0;
     const int64_t plane = nyg * nxg;
@@ -513,7 +530,6 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     if (!(flags & FD_FLAG_ALLOW_UNSTABLE) && ratio > lim)
         return fail(FD_ERR_UNSTABLE, "unstable: max(v)*dt/h = %.6f exceeds the CFL limit %.6f (ratio %.4f)", ratio,
                     lim, ratio / lim);
-    if (nranks > 1 && !nccl().ok) return fail(FD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -531,7 +547,7 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     cudaGetDevice(&c->device);
     cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
     c->pitch = (nxg + 31) / 32 * 32;
-    if (nranks > 1) {
+    if (nranks > 1 && nccl_id) {
         memcpy(&c->nccl_id, nccl_id, sizeof(ncclUniqueId));
         c->have_id = true;
     }
@@ -894,6 +910,8 @@ static fd_status prepare(fd_ctx *c) {
     // per two steps.
     const bool overlap = multi && c->opt_kernel == 0;
     c->overlap = overlap;
+    if (c->opt_transport == 1 && (!multi || c->opt_kernel != 0))
+        return fail(FD_ERR_STATE, "FD_OPT_TRANSPORT=1 needs z-slabs (ranks or FD_OPT_VSLABS) and the fused kernels");
     for (size_t q = 0; q < c->slabs.size(); ++q) {
         Slab &s = c->slabs[q];
         s.has_lo = c->nranks > 1 ? c->rank > 0 : q > 0;
@@ -937,6 +955,7 @@ static fd_status prepare(fd_ctx *c) {
         for (auto &s : c->slabs) {
             const size_t fbytes = (size_t)buf_floats(c, s) * 4;
             for (int b = 2; b < 4; ++b) {
+                if (s.F[b]) continue;                  // fd_peer_export allocated it
                 s.F[b] = (float *)dev_alloc(fbytes);
                 if (!s.F[b]) return fail(FD_ERR_NOMEM, "temporal-blocking buffer allocation failed");
                 CUDA_TRY(c, cudaMemset(s.F[b], 0, fbytes));
@@ -972,7 +991,14 @@ static fd_status prepare(fd_ctx *c) {
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
     }
-    if (c->nranks > 1) {
+    if (c->nranks > 1 && c->opt_transport == 1) {
+        // peer transport: fd_peer_export / fd_peer_import set up the mappings
+        // (the K halos go with the first exchange)
+        if (!c->peer_imported)
+            return fail(FD_ERR_STATE, "FD_OPT_TRANSPORT=1: call fd_peer_export / fd_peer_import before fd_step");
+    } else if (c->nranks > 1) {
+        if (!nccl().ok) return fail(FD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+        if (!c->have_id) return fail(FD_ERR_ARG, "nccl_id is NULL with nranks > 1 (NCCL transport)");
         ncclResult_t r = nccl().CommInitRank(&c->comm, c->nranks, c->nccl_id, c->rank);
         if (r != 0) {
             c->poisoned = true;
@@ -1122,6 +1148,27 @@ static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStrea
             [&] { time_update_kernel<R, NDIM><<<blocks, 256, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });
 }
 
+// In-kernel halo pushes of a boundary launch (FD_OPT_TRANSPORT = 1): buffer b1
+// (pnext) pushes `push1` planes per face, b2 (pnext2, two-step kernels) `push2`.
+static void set_push(const fd_ctx *c, const Slab &s, StepParams &p, int b1, int push1, int b2, int push2) {
+    const size_t q = (size_t)(&s - c->slabs.data());
+    auto one = [&](PeerPush &pp, int b, int push) {
+        pp = PeerPush{nullptr, nullptr, 0, push};
+        if (b < 0) return;
+        if (c->nranks > 1) {
+            pp.lo = s.has_lo ? c->plo.F[b] : nullptr;
+            pp.hi = s.has_hi ? c->phi.F[b] : nullptr;
+            pp.lo_z = (int32_t)(c->plo.nz + c->H);
+        } else {
+            pp.lo = q > 0 ? c->slabs[q - 1].F[b] : nullptr;
+            pp.hi = q + 1 < c->slabs.size() ? c->slabs[q + 1].F[b] : nullptr;
+            pp.lo_z = q > 0 ? (int32_t)(c->slabs[q - 1].nz + c->H) : 0;
+        }
+    };
+    one(p.peer1, b1, push1);
+    one(p.peer2, b2, push2);
+}
+
 static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     StepParams p;
     fill_params(c, s, &g, p, c->k);
@@ -1177,6 +1224,7 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     g.ctas = (int)grid.x;
     const CUtensorMap &mp = s.mHalo[c->icur];
     const CUtensorMap &mpp = s.mTile[c->iprev];
+    if (c->opt_transport == 1 && g.boundary) set_push(c, s, p, c->iprev, c->opt_tsteps == 2 ? c->H : c->R, -1, 0);
     tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
@@ -1266,6 +1314,43 @@ static fd_status resident_steps(fd_ctx *c, int64_t n) {
     return FD_OK;
 }
 
+// Ranks with FD_OPT_TRANSPORT = 1.  peer_signal: after this rank's pushes (the
+// boundary launches or peer_copy) on stream st, publish the exchange count in
+// the neighbours' flags.  peer_wait: before launches that read halos, wait for
+// the neighbours' count of the previous exchange (which also orders our next
+// pushes after their reads of the halos those pushes overwrite).
+static void peer_signal(fd_ctx *c, cudaStream_t st) {
+    ++c->xcount;
+    int64_t *lo = c->rank > 0 ? c->plo.flags + 1 : nullptr;            // rank - 1 hears from its upper side
+    int64_t *hi = c->rank < c->nranks - 1 ? c->phi.flags : nullptr;    // rank + 1 from its lower side
+    peer_signal_kernel<<<1, 1, 0, st>>>(lo, hi, c->xcount);
+    ++c->launches;
+}
+static void peer_wait(fd_ctx *c, cudaStream_t st) {
+    peer_wait_kernel<<<1, 1, 0, st>>>(c->d_flags, c->rank > 0, c->rank < c->nranks - 1, c->xcount);
+    ++c->launches;
+}
+// Push `depth` boundary planes of buffer b (-1: K) into the neighbours' halos
+// with copies (the first exchange: initial fields and the static K halos).
+static fd_status peer_copy(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_t st) {
+    const int64_t pf = plane_floats(c);
+    Slab &s = c->slabs[0];
+    for (const XBuf &x : xs) {
+        const int64_t H = x.b < 0 ? c->R : c->H, d = x.depth;
+        const float *src = x.b < 0 ? s.Kh : s.F[x.b];
+        const size_t bytes = (size_t)(d * pf) * 4;
+        if (c->rank > 0) {
+            float *dst = x.b < 0 ? c->plo.Kh : c->plo.F[x.b];
+            CUDA_TRY(c, cudaMemcpyAsync(dst + (H + c->plo.nz) * pf, src + H * pf, bytes, cudaMemcpyDefault, st));
+        }
+        if (c->rank < c->nranks - 1) {
+            float *dst = x.b < 0 ? c->phi.Kh : c->phi.F[x.b];
+            CUDA_TRY(c, cudaMemcpyAsync(dst + (H - d) * pf, src + (H + s.nz - d) * pf, bytes, cudaMemcpyDefault, st));
+        }
+    }
+    return FD_OK;
+}
+
 static fd_status one_step(fd_ctx *c) {
     fd_status s;
     if (c->overlap) {
@@ -1275,12 +1360,18 @@ static fd_status one_step(fd_ctx *c) {
         // as p; its kernels read the halos received in step k).
         CUDA_TRY(c, cudaEventRecord(c->ev_step, c->stream));
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
+        const bool peer_ranks = c->opt_transport == 1 && c->nranks > 1;
+        if (peer_ranks) peer_wait(c, c->comm_stream);
         for (auto &sl : c->slabs)
             for (auto &g : sl.regions)
                 if (g.boundary) launch_region(c, sl, g, c->comm_stream);
-        const int d = c->opt_tsteps == 2 ? c->H : c->R;     // = the boundary regions' width
-        tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, {{c->iprev, d}}, c->comm_stream); }, false);
-        if (s) return s;
+        if (peer_ranks) peer_signal(c, c->comm_stream);
+        if (c->opt_transport != 1) {
+            const int d = c->opt_tsteps == 2 ? c->H : c->R;     // = the boundary regions' width
+            tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, {{c->iprev, d}}, c->comm_stream); },
+                    false);
+            if (s) return s;
+        }
         CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
         for (auto &sl : c->slabs)
             for (auto &g : sl.regions)
@@ -1323,6 +1414,7 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
+    if (c->opt_transport == 1 && g.boundary) set_push(c, s, p, f1, c->R, f2, c->H);
     tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, m0, mm, s.mKe, p); });
 }
 
@@ -1334,12 +1426,17 @@ static fd_status two_steps(fd_ctx *c) {
     if (c->overlap) {
         CUDA_TRY(c, cudaEventRecord(c->ev_step, c->stream));
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
+        const bool peer_ranks = c->opt_transport == 1 && c->nranks > 1;
+        if (peer_ranks) peer_wait(c, c->comm_stream);
         for (auto &sl : c->slabs)
             for (auto &g : sl.tb2)
                 if (g.boundary) launch_tb2(c, sl, g, f1, f2, c->comm_stream);
-        tracked(c, FD_K_HALO, c->comm_stream,
-                [&] { s = exchange(c, {{f2, c->H}, {f1, c->R}}, c->comm_stream); }, false);
-        if (s) return s;
+        if (peer_ranks) peer_signal(c, c->comm_stream);
+        if (c->opt_transport != 1) {
+            tracked(c, FD_K_HALO, c->comm_stream,
+                    [&] { s = exchange(c, {{f2, c->H}, {f1, c->R}}, c->comm_stream); }, false);
+            if (s) return s;
+        }
         CUDA_TRY(c, cudaEventRecord(c->ev_comm, c->comm_stream));
         for (auto &sl : c->slabs)
             for (auto &g : sl.tb2)
@@ -1544,7 +1641,13 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
             fill_params(c, sl, nullptr, p, c->k - 1);   // w_{(k-1)+1} = w_k
             if (p.nsrc > 0) dispatch_inject(c, c->stream, cur_buf(c, sl), p);
         }
-        if (c->slabs.size() > 1 || c->nranks > 1) {
+        if (c->nranks > 1 && c->opt_transport == 1) {
+            // peer transport: push the initial halos (and K's, once) with copies
+            if (c->opt_tsteps == 2) s = peer_copy(c, {{c->icur, c->H}, {c->iprev, c->R}, {-1, c->R}}, c->stream);
+            else s = peer_copy(c, {{c->icur, c->R}}, c->stream);
+            if (s) return s;
+            peer_signal(c, c->stream);
+        } else if (c->slabs.size() > 1 || c->nranks > 1) {
             // halos of P (2r for temporal blocking) and, for temporal
             // blocking, r of P_prev (fd_set_wavefield may have set it)
             if (c->opt_tsteps == 2) s = exchange(c, {{c->icur, c->H}, {c->iprev, c->R}}, c->stream);
@@ -1651,6 +1754,104 @@ fd_status fd_get_traces(fd_ctx *c, float *host_out, int64_t cap, int64_t *nsteps
     return FD_OK;
 }
 
+// ---- peer transport (include/fd.h): IPC handles of the field buffers, K, flags
+struct PeerBlob {
+    uint32_t magic, version;
+    int64_t nz, nxg, nyg, nzg;
+    int32_t H, rank, nbuf, pad;
+    cudaIpcMemHandle_t F[4], Kh, flags;
+};
+static_assert(sizeof(PeerBlob) <= FD_PEER_BLOB_BYTES, "peer blob size");
+constexpr uint32_t kPeerMagic = 0x46445042u;   // "FDPB"
+
+fd_status fd_peer_export(fd_ctx *c, void *blob, size_t cap, size_t *len) {
+    fd_status s = check_ctx(c);
+    if (s) return s;
+    if (!blob || !len) return fail(FD_ERR_ARG, "blob/len is NULL");
+    if (cap < sizeof(PeerBlob)) return fail(FD_ERR_ARG, "cap %zu < %zu", cap, sizeof(PeerBlob));
+    if (c->nranks < 2 || c->opt_transport != 1)
+        return fail(FD_ERR_STATE, "fd_peer_export needs a multi-rank context with FD_OPT_TRANSPORT=1");
+    if (c->peer_imported || c->started) return fail(FD_ERR_STATE, "fd_peer_export after fd_peer_import / fd_step");
+    if (g_alloc) return fail(FD_ERR_STATE, "FD_OPT_TRANSPORT=1 needs the default allocator (CUDA IPC)");
+    // all four field buffers (the two-step kernels' too) and the flags exist
+    // from here on; the options are frozen (the mappings depend on them)
+    Slab &ss = c->slabs[0];
+    const size_t fbytes = (size_t)buf_floats(c, ss) * 4;
+    for (int b = 2; b < 4; ++b) {
+        if (ss.F[b]) continue;
+        ss.F[b] = (float *)dev_alloc(fbytes);
+        if (!ss.F[b]) return fail(FD_ERR_NOMEM, "field buffer allocation failed");
+        CUDA_TRY(c, cudaMemset(ss.F[b], 0, fbytes));
+        c->dev_bytes += (double)fbytes;
+    }
+    if (!c->d_flags) {
+        CUDA_TRY(c, cudaMalloc(&c->d_flags, 2 * sizeof(int64_t)));
+        CUDA_TRY(c, cudaMemset(c->d_flags, 0, 2 * sizeof(int64_t)));
+    }
+    c->frozen = true;
+    // buffers zeroed / uploaded before any neighbour may write their halos
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    PeerBlob b;
+    memset(&b, 0, sizeof b);
+    b.magic = kPeerMagic; b.version = 1;
+    const Slab &sl = c->slabs[0];
+    b.nz = sl.nz; b.nxg = c->nxg; b.nyg = c->nyg; b.nzg = c->nzg;
+    b.H = c->H; b.rank = c->rank;
+    for (int i = 0; i < 4 && sl.F[i]; ++i, ++b.nbuf) CUDA_TRY(c, cudaIpcGetMemHandle(&b.F[i], sl.F[i]));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&b.Kh, sl.Kh));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&b.flags, c->d_flags));
+    memcpy(blob, &b, sizeof b);
+    *len = sizeof b;
+    return FD_OK;
+}
+
+fd_status fd_peer_import(fd_ctx *c, const void *lo_blob, const void *hi_blob) {
+    fd_status s = check_ctx(c);
+    if (s) return s;
+    if (c->nranks < 2 || c->opt_transport != 1 || !c->frozen || c->started)
+        return fail(FD_ERR_STATE, "fd_peer_import needs fd_peer_export first (FD_OPT_TRANSPORT=1, nranks > 1)");
+    if (c->peer_imported) return fail(FD_ERR_STATE, "fd_peer_import called twice");
+    if ((c->rank > 0) != (lo_blob != nullptr) || (c->rank < c->nranks - 1) != (hi_blob != nullptr))
+        return fail(FD_ERR_ARG, "rank %d needs %s lower and %s upper blob", c->rank, c->rank > 0 ? "a" : "no",
+                    c->rank < c->nranks - 1 ? "an" : "no");
+    int nbuf = 0;
+    while (nbuf < 4 && c->slabs[0].F[nbuf]) ++nbuf;
+    auto open = [&](const void *raw, int want_rank, fd_ctx::Peer &pr) -> fd_status {
+        PeerBlob b;
+        memcpy(&b, raw, sizeof b);
+        if (b.magic != kPeerMagic || b.version != 1 || b.nxg != c->nxg || b.nyg != c->nyg || b.nzg != c->nzg ||
+            b.H != c->H || b.rank != want_rank || b.nbuf != nbuf)
+            return fail(FD_ERR_STATE, "peer blob does not match this grid / rank %d", want_rank);
+        auto map = [&](const cudaIpcMemHandle_t &h, void **out) -> fd_status {
+            cudaError_t e = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(FD_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+            }
+            pr.opened.push_back(*out);
+            return FD_OK;
+        };
+        void *p = nullptr;
+        for (int i = 0; i < nbuf; ++i) {
+            fd_status st = map(b.F[i], &p);
+            if (st) return st;
+            pr.F[i] = (float *)p;
+        }
+        fd_status st = map(b.Kh, &p);
+        if (st) return st;
+        pr.Kh = (float *)p;
+        st = map(b.flags, &p);
+        if (st) return st;
+        pr.flags = (int64_t *)p;
+        pr.nz = b.nz;
+        return FD_OK;
+    };
+    if (lo_blob) { s = open(lo_blob, c->rank - 1, c->plo); if (s) return s; }
+    if (hi_blob) { s = open(hi_blob, c->rank + 1, c->phi); if (s) return s; }
+    c->peer_imported = true;
+    return FD_OK;
+}
+
 fd_status fd_destroy(fd_ctx *c) {
     if (!c) return FD_OK;
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -1725,7 +1926,8 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         c->opt_profile = v ? 1 : 0;
         return FD_OK;
     }
-    if (c->started) return fail(FD_ERR_STATE, "option %d only before the first fd_step", key);
+    if (c->started || c->frozen)
+        return fail(FD_ERR_STATE, "option %d only before the first fd_step / fd_peer_export", key);
     switch (key) {
     case FD_OPT_KERNEL:
         if (v < 0 || v > 3) return fail(FD_ERR_ARG, "FD_OPT_KERNEL must be 0, 1, 2 or 3");
@@ -1754,6 +1956,10 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         c->opt_tb2tile = (int)v;
         return FD_OK;
     case FD_OPT_GRAPH: c->opt_graph = v ? 1 : 0; return FD_OK;
+    case FD_OPT_TRANSPORT:
+        if (v != 0 && v != 1) return fail(FD_ERR_ARG, "FD_OPT_TRANSPORT must be 0 or 1");
+        c->opt_transport = (int)v;
+        return FD_OK;
     case FD_OPT_RESIDENT:
         if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_RESIDENT must be 0, 1 or 2");
         c->opt_resident = (int)v;

@@ -18,7 +18,7 @@
 //
 // Buffers: four field buffers rotate (cur, prev) -> (C, D); none is written
 // while another CTA may still read it (P^k and P^{k-1} are read with halos).
-// Single-slab contexts only (slabs would need 2r-deep halos).
+// On z-slabs the halos are 2r planes of P^k and r of P^{k-1} (fd_runtime.cu).
 #pragma once
 #include "fd_kernels.cuh"
 
@@ -222,8 +222,10 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         }
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (store && interior && xb < (int)prm.pitch)
+                    if (store && interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + halo_planes(R)) * ny + y) * prm.pitch + xb) = o;
+                        peer_store4<R>(prm.peer1, z1, (int)prm.nz, (int64_t)ny * prm.pitch, (int64_t)y * prm.pitch + xb, o);
+                    }
                 }
             }
             if (store && rz == z1) {                              // owners: tile-interior A threads
@@ -371,7 +373,11 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float *dst = prm.pnext2 + ((int64_t)(z2 + halo_planes(R)) * ny + y0 + ri0) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
-                if (y0 + ri0 + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if (y0 + ri0 + yy < ny) {
+                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                    peer_store4<R>(prm.peer2, z2, (int)prm.nz, (int64_t)ny * prm.pitch,
+                                   (int64_t)(y0 + ri0 + yy) * prm.pitch + xb, out[yy]);
+                }
         }
     }
 }
@@ -517,8 +523,10 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         }
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (interior && xb < (int)prm.pitch)
+                    if (interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + halo_planes(R)) * prm.pitch + xb) = o;
+                        peer_store4<R>(prm.peer1, z, (int)prm.nz, prm.pitch, xb, o);
+                    }
                 }
             }
             if (rp < rend && prm.rec.z[rp] < rb + C::TY)              // owners: block-interior A threads
@@ -614,7 +622,10 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             float *dst = prm.pnext2 + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
-                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if (zt + yy < prm.zhi) {
+                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                    peer_store4<R>(prm.peer2, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
+                }
         }
     }
 }

@@ -33,11 +33,21 @@ def bootstrap_nccl_id(make_id=None) -> bytes:
 
 def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *, device: int = -1,
            nccl_id: bytes | None = None, flags: int = 0, options: dict | None = None,
-           stream: int | None = None) -> "_fd.Simulation":
-    """Create this rank's slab context; ``vel_slab`` holds only the owned planes."""
+           stream: int | None = None, transport: str = "nccl") -> "_fd.Simulation":
+    """Create this rank's slab context; ``vel_slab`` holds only the owned planes.
+
+    ``transport``: "nccl" (halo send/recv on the library's comm stream) or
+    "peer" (FD_OPT_TRANSPORT=1: the boundary launches store their planes into
+    the neighbours' halos through CUDA IPC mappings; this function exchanges
+    the IPC blobs with torch.distributed)."""
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
-    if nccl_id is None and world > 1:
+    if transport not in ("nccl", "peer"):
+        raise ValueError(f"transport must be 'nccl' or 'peer', not {transport!r}")
+    peer = transport == "peer" and world > 1
+    if peer:
+        options = {**(options or {}), _fd.FD_OPT_TRANSPORT: 1}
+    elif nccl_id is None and world > 1:
         nccl_id = bootstrap_nccl_id()
     sim, err = None, None
     try:
@@ -53,6 +63,23 @@ def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *
         if sim is not None:
             sim.close()
         raise err if err is not None else RuntimeError("fd_create_dist failed on another rank")
+    if peer:
+        blob, err = None, None
+        try:
+            blob = _fd.fd_peer_export(sim.ctx)
+        except _fd.FDError as e:
+            err = e
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        if err is None and all(b is not None for b in blobs):
+            try:
+                _fd.fd_peer_import(sim.ctx, blobs[rank - 1] if rank > 0 else None,
+                                   blobs[rank + 1] if rank < world - 1 else None)
+            except _fd.FDError as e:
+                err = e
+        if not all_ok(err is None):
+            sim.close()
+            raise err if err is not None else RuntimeError("peer transport setup failed on another rank")
     return sim
 
 

@@ -23,7 +23,8 @@ FD_FLAG_ALLOW_UNSTABLE = 1
 FD_OPT_KERNEL, FD_OPT_TILE, FD_OPT_ZCHUNKS, FD_OPT_ASYNC, FD_OPT_GRAPH, FD_OPT_VSLABS = 1, 2, 3, 4, 5, 6
 FD_OPT_PROFILE = 7
 FD_OPT_TSTEPS, FD_OPT_TB2TILE, FD_OPT_RESERVE = 8, 9, 10
-FD_OPT_RESIDENT, FD_OPT_CLUSTER = 11, 12
+FD_OPT_RESIDENT, FD_OPT_CLUSTER, FD_OPT_TRANSPORT = 11, 12, 13
+FD_PEER_BLOB_BYTES = 512
 KERNEL_KINDS = ["fused", "naive", "gather", "inject", "fd_pxx", "fd_pyy", "fd_pzz", "fd_time", "halo",
                 "resident"]
 
@@ -32,6 +33,7 @@ EXPORTED = [
     "fd_set_receivers", "fd_step", "fd_get_wavefield", "fd_get_traces", "fd_destroy",
     "fd_strerror", "fd_last_error", "fd_set_stream", "fd_set_allocator", "fd_set_wavefield",
     "fd_set_option", "fd_get_info", "fd_get_kernel_times", "fd_reset_kernel_times",
+    "fd_peer_export", "fd_peer_import",
 ]
 
 
@@ -99,6 +101,8 @@ def _load() -> ctypes.CDLL:
         "fd_get_info": ([ctypes.c_void_p, ctypes.POINTER(FdInfo)], st),
         "fd_get_kernel_times": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), _i64p], st),
         "fd_reset_kernel_times": ([ctypes.c_void_p], st),
+        "fd_peer_export": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], st),
+        "fd_peer_import": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -162,6 +166,20 @@ def fd_nccl_get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib.fd_nccl_get_unique_id(buf), "fd_nccl_get_unique_id")
     return buf.raw
+
+
+def fd_peer_export(ctx) -> bytes:
+    """IPC handles of this rank's field buffers, K and flags (FD_OPT_TRANSPORT=1)."""
+    buf = ctypes.create_string_buffer(FD_PEER_BLOB_BYTES)
+    n = ctypes.c_size_t()
+    _check(lib.fd_peer_export(ctx, buf, FD_PEER_BLOB_BYTES, ctypes.byref(n)), "fd_peer_export")
+    return buf.raw[:n.value]
+
+
+def fd_peer_import(ctx, lo_blob: bytes | None, hi_blob: bytes | None):
+    lo = ctypes.create_string_buffer(lo_blob, len(lo_blob)) if lo_blob else None
+    hi = ctypes.create_string_buffer(hi_blob, len(hi_blob)) if hi_blob else None
+    _check(lib.fd_peer_import(ctx, lo, hi), "fd_peer_import")
 
 
 def fd_add_source(ctx, idx, f_peak_hz: float, t0_s: float, amp: float = 1.0):

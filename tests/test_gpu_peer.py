@@ -1,0 +1,117 @@
+"""Peer transport (FD_OPT_TRANSPORT=1): halo planes stored by the
+step kernels straight into the neighbouring slab's buffers.
+
+* virtual slabs (one process): bitwise equal to one slab, single steps and
+  two steps per launch, 2D and 3D;
+* two processes on the one GPU of this run (torch.distributed.run, gloo for the
+  plumbing, CUDA IPC mappings + flag sync for the data path -- the multi-rank
+  code path without NCCL): bitwise equal to one process.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import _rand_vel, run_gpu
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2311_05038_b200.build import build_lib
+    build_lib()
+    import paper_2311_05038_b200 as m
+    return m
+
+
+@pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((41, 29, 66), 4), ((45, 26, 50), 8),
+                                        ((96, 300), 2), ((70, 140), 8)])
+@pytest.mark.parametrize("nslabs", [2, 3])
+@pytest.mark.parametrize("tsteps", [1, 2])
+def test_peer_virtual_slabs_bitwise(fd, dims, order, nslabs, tsteps):
+    if tsteps == 2 and len(dims) == 3 and order > 4:
+        pytest.skip("two-step kernel: 3D r <= 2")
+    vel = _rand_vel(dims, seed=73)
+    r = order // 2
+    nz = dims[0]
+    from paper_2311_05038_b200.dist import partition
+    f1 = partition(nz, nslabs, 1)[0]
+    rest = tuple(d // 2 for d in dims[1:])
+    src = [((f1,) + rest, 25.0, 0.02, 1.0), ((f1 - r,) + rest, 15.0, 0.03, -0.4)]
+    recs = [(f1 - 1,) + rest, (f1,) + rest, (f1 + 2 * r - 1,) + rest, (nz - 3,) + rest]
+    ref = run_gpu(fd, vel, 10.0, 5e-4, order, 33, src, recs, options={fd.FD_OPT_TSTEPS: 1})
+    for graph in (1, 0):
+        got = run_gpu(fd, vel, 10.0, 5e-4, order, 33, src, recs,
+                      options={fd.FD_OPT_VSLABS: nslabs, fd.FD_OPT_TRANSPORT: 1, fd.FD_OPT_TSTEPS: tsteps,
+                               fd.FD_OPT_GRAPH: graph})
+        for a, b in zip(got[:3], ref[:3]):
+            assert np.array_equal(a, b), (nslabs, tsteps, graph)
+
+
+def test_peer_transport_needs_slabs(fd):
+    vel = _rand_vel((20, 20, 20), seed=1)
+    with pytest.raises(fd.FDError) as e:
+        with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_TRANSPORT: 1, fd.FD_OPT_RESIDENT: 1}) as sim:
+            sim.step(1)
+    assert e.value.status == fd.FD_ERR_STATE
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("peer_worker", os.path.join(ROOT, "tests", "peer_worker.py"))
+    worker = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(worker)
+    out = str(tmp_path / "peer.npz")
+    port = 29600 + nranks + (os.getpid() % 200)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "peer_worker.py"),
+           out]
+    env = {**os.environ, "PYTHONPATH": ROOT}
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    got = np.load(out)
+    for ci, (dims, order, seq) in enumerate(worker.CASES):
+        vel = np.random.default_rng(ci).uniform(1500, 2500, dims).astype(np.float32)
+        rest = tuple(d // 2 for d in dims[1:])
+        from paper_2311_05038_b200.dist import partition
+        f1 = partition(dims[0], nranks, 1)[0]
+        src = [((f1,) + rest, 25.0, 0.02, 1.0), ((f1 - 1,) + rest, 15.0, 0.03, -0.5)]
+        recs = [(f1 - 1,) + rest, (f1,) + rest, (dims[0] - 3,) + rest]
+        with fd.Simulation(vel, 10.0, 5e-4, order, options={fd.FD_OPT_RESIDENT: 1, fd.FD_OPT_TSTEPS: 1}) as sim:
+            for s in src:
+                sim.add_source(*s)
+            sim.set_receivers(recs)
+            for n in seq:
+                sim.step(n)
+            ref = (sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces())
+        assert np.array_equal(got[f"P{ci}"], ref[0]), ci
+        assert np.array_equal(got[f"Pp{ci}"], ref[1]), ci
+        assert np.array_equal(got[f"T{ci}"], ref[2]), ci
+
+
+def test_bench_two_ranks_peer_transport_shared_gpu(fd):
+    """bench.py's N>1 path end to end (torchrun, barriers, max over ranks, e2e,
+    one JSON line from rank 0) with the peer transport, both ranks on the one
+    GPU of this run (FD_BENCH_SHARE_GPU test hook; not a scaling number)."""
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(29800 + os.getpid() % 100), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "20", "--warmup", "3", "--config", "C1", "--transport", "peer",
+           "--no-cpu-baseline"]
+    env = {**os.environ, "FD_BENCH_SHARE_GPU": "1", "PYTHONPATH": ROOT}
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["traces_finite"]
+    assert d["config"]["global_grid"][0] == 2 * d["config"]["grid"][0]
+    assert "peer" in d["config"]["parallelism"] and d["config"]["shared_gpu"]
