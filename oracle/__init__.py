@@ -12,7 +12,7 @@ only marshals numpy arrays.
 
 Parity status per function (DESIGN.md section 4 lists the pins):
   coefficients, cfl_max, ricker, second_derivative, time_update, run,
-  run_slabs: pinned (tests/test_oracle_pins.py).
+  run_slabs, sponge_profile, run(sponge=...): pinned (tests/test_oracle_pins.py).
 """
 from __future__ import annotations
 
@@ -63,6 +63,8 @@ def lib() -> ctypes.CDLL:
                     ctypes.c_int, _i64p, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.c_int]
         _lib.oracle_run.argtypes = run_args
         _lib.oracle_run_slabs.argtypes = run_args
+        _lib.oracle_run_sponge.argtypes = run_args + [ctypes.c_int, ctypes.c_double]
+        _lib.oracle_sponge_profile.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_double, _f64p]
         _lib.oracle_partition.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _i64p, _i64p]
         _lib.oracle_max_threads.restype = ctypes.c_int
     return _lib
@@ -127,14 +129,24 @@ def _pack_sources(sources, ndim):
     return n, idx, f, t0, amp
 
 
+def sponge_profile(n: int, nb: int, alpha: float) -> np.ndarray:
+    """Cerjan damping profile g(j), j = 0..n-1 (R#18; fd_oracle.c)."""
+    g = np.zeros(int(n))
+    if lib().oracle_sponge_profile(int(n), int(nb), float(alpha), _p(g, _f64p)) != 0:
+        raise ValueError("bad sponge profile args")
+    return g
+
+
 def run(vel, h, dt, order, nt, sources=(), receivers=(), P0=None, Pm1=None,
-        nthreads: int = 1, nranks: int = 0):
+        nthreads: int = 1, nranks: int = 0, sponge=None):
     """Run ``nt`` steps; returns (P^nt, P_mod^{nt-1}, traces[nrec, nt]).
 
     ``vel``: velocity array (shape = grid, slow->fast); its values are used in
     fp64 exactly as given (pass the fp32 model to compare with the GPU path).
     ``sources``: list of (idx, f_peak, t0, amp); ``receivers``: list of idx.
     ``nranks`` > 0 selects the z-slab mode (bitwise equal by construction).
+    ``sponge`` = (nb, alpha) selects the Cerjan absorbing frame (R#18;
+    oracle_run_sponge; the returned Pold is the stored P^{nt-1}).
     """
     V = np.ascontiguousarray(vel, dtype=np.float64)
     ndim = V.ndim
@@ -147,11 +159,16 @@ def run(vel, h, dt, order, nt, sources=(), receivers=(), P0=None, Pm1=None,
     T = np.zeros((max(nrec, 1), max(int(nt), 1)))
     recs_c = np.ascontiguousarray(recs if nrec else np.zeros((1, ndim), np.int64))
     L = lib()
-    fn = L.oracle_run_slabs if nranks > 0 else L.oracle_run
-    last = nranks if nranks > 0 else int(nthreads)
-    rc = fn(ndim, _p(dims, _i64p), float(h), float(dt), int(order), _p(V, _f64p),
+    args = (ndim, _p(dims, _i64p), float(h), float(dt), int(order), _p(V, _f64p),
             ns, _p(sidx, _i64p), _p(sf, _f64p), _p(st0, _f64p), _p(samp, _f64p),
-            nrec, _p(recs_c, _i64p), int(nt), _p(P, _f64p), _p(Pold, _f64p), _p(T, _f64p), last)
+            nrec, _p(recs_c, _i64p), int(nt), _p(P, _f64p), _p(Pold, _f64p), _p(T, _f64p))
+    if sponge is not None:
+        if nranks > 0:
+            raise ValueError("the sponge oracle has no slab mode")
+        rc = L.oracle_run_sponge(*args, int(nthreads), int(sponge[0]), float(sponge[1]))
+    else:
+        fn = L.oracle_run_slabs if nranks > 0 else L.oracle_run
+        rc = fn(*args, nranks if nranks > 0 else int(nthreads))
     if rc != 0:
         raise ValueError(f"oracle run failed ({rc})")
     return P, Pold, T[:nrec, :int(nt)]

@@ -279,6 +279,107 @@ int oracle_run(int ndim, const int64_t *dims, double h, double dt, int order,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Absorbing sponge boundary (reading R#18).  The paper is    */
+/* silent on boundaries (R#3) and SPEC lists absorbing boundaries as a         */
+/* non-goal; this is the optional alternative to the band rule alone. */
+/* Cerjan et al. (1985, Geophysics 50:705): after each step, multiply the new */
+/* and the current field by G inside a frame of nb cells, with                */
+/*   g(j) = exp(-(alpha * (nb - d))^2),  d = min(j, n-1-j) < nb; else 1       */
+/* per axis and G(i) = g_z(i_z) * g_y(i_y) * g_x(i_x).  Written for the       */
+/* STORED fields (P as it enters the next step, i.e. Cerjan's damped P^{k+1}  */
+/* plus the next injection; Pold = P^{k-1} as stored one step earlier):       */
+/* Cerjan's Pold for step k is G * (stored P^{k-1}), so the step is            */
+/*   Pnew = G * (2 P - G * Pold + dt^2 V^2 (Pxx [+ Pyy] + Pzz))               */
+/* and the stored Pnew is Cerjan's damped P^{k+1} (equivalence checked in      */
+/* tests/test_oracle_pins.py against the damp-after-step form).  The band rule */
+/* still applies to the derivatives.  nb = 0 gives G = 1: the plain scheme.   */
+/* ------------------------------------------------------------------------ */
+int oracle_sponge_profile(int64_t n, int nb, double alpha, double *g)
+{
+    if (n < 1 || nb < 0 || !g) return ORC_ERR_ARG;
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t d = j < n - 1 - j ? j : n - 1 - j;
+        if (d < nb) {
+            const double a = alpha * (double)(nb - d);
+            g[j] = exp(-(a * a));
+        } else {
+            g[j] = 1.0;
+        }
+    }
+    return ORC_OK;
+}
+
+int oracle_run_sponge(int ndim, const int64_t *dims, double h, double dt, int order,
+                      const double *V,
+                      int nsrc, const int64_t *src_idx, const double *src_f,
+                      const double *src_t0, const double *src_amp,
+                      int nrec, const int64_t *rec_idx,
+                      int64_t nt, double *P, double *Pold, double *T, int nthreads,
+                      int nb, double alpha)
+{
+    grid_t g;
+    double c[5];
+    const int r = order / 2;
+    if (!V || !P || !Pold || nt < 0 || h <= 0.0 || dt <= 0.0 || order % 2 || nb < 0 ||
+        make_grid(ndim, dims, &g) || oracle_coefficients(r, c) || nsrc < 0 || nrec < 0)
+        return ORC_ERR_ARG;
+    if (nthreads < 1) nthreads = 1;
+    int64_t *sl = calloc((size_t)(nsrc + 1), sizeof(int64_t));
+    int64_t *rl = calloc((size_t)(nrec + 1), sizeof(int64_t));
+    if (!sl || !rl) { free(sl); free(rl); return ORC_ERR_NOMEM; }
+    for (int s = 0; s < nsrc; ++s)
+        if (lin_index(&g, src_idx + (int64_t)s * ndim, &sl[s])) { free(sl); free(rl); return ORC_ERR_RANGE; }
+    for (int j = 0; j < nrec; ++j)
+        if (lin_index(&g, rec_idx + (int64_t)j * ndim, &rl[j])) { free(sl); free(rl); return ORC_ERR_RANGE; }
+
+    const size_t bytes = (size_t)g.npts * sizeof(double);
+    double *Pxx = malloc(bytes), *Pzz = malloc(bytes);
+    double *Pyy = (ndim == 3) ? malloc(bytes) : NULL;
+    double *Pnew = malloc(bytes), *G = malloc(bytes);
+    double *gx = malloc((size_t)g.n[0] * sizeof(double)), *gy = malloc((size_t)g.n[1] * sizeof(double));
+    double *gz = malloc((size_t)g.n[2] * sizeof(double));
+    if (!Pxx || !Pzz || !Pnew || !G || !gx || !gy || !gz || (ndim == 3 && !Pyy)) {
+        free(Pxx); free(Pzz); free(Pyy); free(Pnew); free(G); free(gx); free(gy); free(gz); free(sl); free(rl);
+        return ORC_ERR_NOMEM;
+    }
+    /* the damping factor per point: the product of the per-axis profiles */
+    oracle_sponge_profile(g.n[0], nb, alpha, gx);
+    oracle_sponge_profile(g.n[2], nb, alpha, gz);
+    if (ndim == 3) oracle_sponge_profile(g.n[1], nb, alpha, gy);
+    else gy[0] = 1.0;
+    for (int64_t iz = 0; iz < g.n[2]; ++iz)
+        for (int64_t iy = 0; iy < g.n[1]; ++iy)
+            for (int64_t ix = 0; ix < g.n[0]; ++ix)
+                G[(iz * g.n[1] + iy) * g.n[0] + ix] = gz[iz] * gy[iy] * gx[ix];
+
+    double *cur = P, *old = Pold, *nxt = Pnew;
+    const double dt2 = dt * dt;
+    for (int64_t k = 0; k < nt; ++k) {
+        for (int s = 0; s < nsrc; ++s)
+            cur[sl[s]] += src_amp[s] * oracle_ricker((double)k * dt, src_f[s], src_t0[s]);
+        second_derivative(&g, 2, r, c, h, cur, Pzz, nthreads);
+        if (ndim == 3) second_derivative(&g, 1, r, c, h, cur, Pyy, nthreads);
+        second_derivative(&g, 0, r, c, h, cur, Pxx, nthreads);
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+#endif
+        for (int64_t i = 0; i < g.npts; ++i) {
+            const double lap = Pyy ? (Pxx[i] + Pyy[i]) + Pzz[i] : Pxx[i] + Pzz[i];
+            nxt[i] = G[i] * (2.0 * cur[i] - G[i] * old[i] + dt2 * V[i] * V[i] * lap);
+        }
+        double *t = old; old = cur; cur = nxt; nxt = t;
+        for (int j = 0; j < nrec; ++j)
+            T[(int64_t)j * nt + k] = cur[rl[j]];
+    }
+    memcpy(Pxx, cur, bytes);
+    memcpy(Pzz, old, bytes);
+    memcpy(P, Pxx, bytes);
+    memcpy(Pold, Pzz, bytes);
+    free(Pxx); free(Pzz); free(Pyy); free(Pnew); free(G); free(gx); free(gy); free(gz); free(sl); free(rl);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Slab mode: the same recursion on nranks z-slabs,    */
 /* each holding its own planes plus r halo planes per side, the halos         */
 /* refreshed by plain memcpy from the neighbour slab after every step.  Used   */

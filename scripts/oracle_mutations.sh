@@ -26,5 +26,11 @@ run_mut "c[0] = -205.0 / 72.0;" "c[0] = -205.0 / 71.0;"
 run_mut "return (1.0 - 2.0 * a) * exp(-a);" "return (1.0 - a) * exp(-a);"
 run_mut "out[i] = acc / h2;" "out[i] = acc / h;"
 run_mut "double *t = old; old = cur; cur = nxt; nxt = t;" "double *t = old; old = nxt; nxt = t;"
+# sponge frame (R#18)
+run_mut "const int64_t d = j < n - 1 - j ? j : n - 1 - j;" "const int64_t d = j < n - j ? j : n - j;"
+run_mut "nxt[i] = G[i] * (2.0 * cur[i] - G[i] * old[i]" "nxt[i] = G[i] * (2.0 * cur[i] - old[i]"
+run_mut "nxt[i] = G[i] * (2.0 * cur[i]" "nxt[i] = (2.0 * cur[i]"
+run_mut "g[j] = exp(-(a * a));" "g[j] = exp(-a);"
+run_mut "= gz[iz] * gy[iy] * gx[ix];" "= gz[iz] * gx[ix];"
 cp /tmp/fd_oracle_orig.c oracle/fd_oracle.c
 python -c "import oracle; oracle.build(force=True)"

@@ -554,3 +554,104 @@ def test_green_function_3d():
     err0 = np.linalg.norm(T[0][win] - ana_noshift[win]) / np.linalg.norm(ana[win])
     assert err < 2e-3, err
     assert err0 > 10 * err
+
+
+# ---------------------------------------------------------------------------
+# Absorbing sponge frame (Cerjan et al. 1985)
+# ---------------------------------------------------------------------------
+def test_sponge_profile_cerjan_values_and_shape():
+    """Cerjan's frame: 20 cells, alpha = 0.015 -> G = exp(-0.09) = 0.9139 at the
+    outermost cell (the value quoted with the method), 1 from the 20th cell
+    in; symmetric; increasing inwards; Gaussian in the depth (nb - d)."""
+    n, nb, a = 101, 20, 0.015
+    g = oracle.sponge_profile(n, nb, a)
+    assert abs(g[0] - 0.91393) < 1e-5 and abs(g[-1] - g[0]) == 0.0
+    assert np.array_equal(g, g[::-1])
+    assert np.all(g[nb:n - nb] == 1.0) and np.all(g[:nb] < 1.0)
+    assert np.all(np.diff(g[:nb + 1]) > 0)
+    depth = nb - np.arange(nb)
+    # ln g is -(a * depth)^2: ratios of logs are ratios of squared depths
+    assert np.allclose(np.log(g[:nb]) / np.log(g[0]), (depth / nb) ** 2, rtol=1e-12)
+    assert np.all(oracle.sponge_profile(n, 0, a) == 1.0)
+
+
+@pytest.mark.parametrize("ndim,order", [(2, 2), (3, 4)])
+def test_sponge_zero_width_is_the_band_rule(ndim, order):
+    dims = (30, 34) if ndim == 2 else (20, 22, 24)
+    vel = np.random.default_rng(3).uniform(1500, 2500, dims)
+    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0)]
+    recs = [tuple(d // 3 for d in dims)]
+    a = oracle.run(vel, 10.0, 1e-3, order, 25, src, recs)
+    b = oracle.run(vel, 10.0, 1e-3, order, 25, src, recs, sponge=(0, 0.015))
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_sponge_v0_closed_form():
+    """V = 0: each point obeys P^{k+1} = G (2 P^k - G P^{k-1}); from P^0 = P^-1 = c
+    the solution is P^k = c (1 + (1 - G) k) G^k (double root G).  Catches a
+    missing inner or outer G and a wrong per-axis product."""
+    dims, nb, a, c = (17, 19, 23), 6, 0.08, 0.37
+    P0 = np.full(dims, c)
+    G = (oracle.sponge_profile(dims[0], nb, a)[:, None, None] * oracle.sponge_profile(dims[1], nb, a)[None, :, None]
+         * oracle.sponge_profile(dims[2], nb, a)[None, None, :])
+    for k in (1, 2, 7):
+        P, Pold, _ = oracle.run(np.zeros(dims), 10.0, 1e-3, 2, k, P0=P0, Pm1=P0, sponge=(nb, a))
+        assert np.allclose(P, c * (1 + (1 - G) * k) * G ** k, rtol=1e-13, atol=0)
+        assert np.allclose(Pold, c * (1 + (1 - G) * (k - 1)) * G ** (k - 1), rtol=1e-13, atol=0)
+    assert G.min() < 0.7                       # the test exercises real damping
+
+
+def test_sponge_equals_cerjan_damp_after_step():
+    """The stored-field step of the oracle is Cerjan's algorithm: run the
+    original form -- update, then multiply the new AND the current field by G
+    -- with the oracle's pinned derivative operator and compare."""
+    dims, h, dt, order, nb, a, nt = (44, 52), 10.0, 1e-3, 4, 9, 0.05, 40
+    vel = np.random.default_rng(5).uniform(1800, 2600, dims)
+    src = [((20, 30), 25.0, 0.02, 1.0), ((9, 11), 18.0, 0.03, -0.6)]     # one source inside the frame
+    recs = [(22, 26), (4, 5), (40, 48)]
+    P, Pold, T = oracle.run(vel, h, dt, order, nt, src, recs, sponge=(nb, a))
+    G = oracle.sponge_profile(dims[0], nb, a)[:, None] * oracle.sponge_profile(dims[1], nb, a)[None, :]
+    cur, old = np.zeros(dims), np.zeros(dims)
+    Tc = np.zeros((len(recs), nt))
+    for k in range(nt):
+        for idx, f, t0, amp in src:
+            cur[idx] += amp * oracle.ricker(k * dt, f, t0)
+        lap = oracle.second_derivative(cur, h, order, "x") + oracle.second_derivative(cur, h, order, "z")
+        new = 2 * cur - old + dt * dt * vel * vel * lap
+        new, cur = G * new, G * cur                       # Cerjan: damp both time levels
+        old, cur = cur, new
+        for j, q in enumerate(recs):
+            Tc[j, k] = cur[q]
+    assert np.allclose(P, cur, rtol=0, atol=1e-12 * np.abs(cur).max())
+    assert np.allclose(G * Pold, old, rtol=0, atol=1e-12 * np.abs(old).max())
+    assert np.allclose(T, Tc, rtol=0, atol=1e-12 * np.abs(Tc).max())
+
+
+def test_sponge_mirror_symmetry_bitexact():
+    n, order = 41, 4
+    vel = np.full((n, n), 2000.0)
+    P, Pold, _ = oracle.run(vel, 10.0, 1e-3, order, 80, [((n // 2, n // 2), 25.0, 0.03, 1.0)], sponge=(8, 0.06))
+    for X in (P, Pold):
+        assert np.array_equal(X, X[::-1, :]) and np.array_equal(X, X[:, ::-1]) and np.array_equal(X, X.T)
+
+
+def test_sponge_absorbs_the_boundary_reflection():
+    """Homogeneous 2D model, receiver near the source: after the direct wave
+    has passed, the band rule alone returns the boundary reflection at full
+    strength (rigid frame); Cerjan's 20-cell frame cuts it by more than 10x."""
+    n, h, v, dt, f = 201, 10.0, 2000.0, 1e-3, 25.0
+    c = n // 2
+    vel = np.full((n, n), v)
+    src = [((c, c), f, 0.04, 1.0)]
+    rec = [(c, c + 10)]
+    nt = 1300
+    _, _, T0 = oracle.run(vel, h, dt, 2, nt, src, rec, nthreads=oracle.max_threads())
+    _, _, T1 = oracle.run(vel, h, dt, 2, nt, src, rec, nthreads=oracle.max_threads(), sponge=(20, 0.015))
+    t = (np.arange(nt) + 1) * dt
+    direct = t < 0.25
+    refl = (t > 0.7) & (t < 1.3)        # first reflections: ~0.9-1.0 s round trip to the nearest faces
+    assert np.allclose(T0[0][direct], T1[0][direct], rtol=0, atol=1e-9 * np.abs(T0).max())
+    r0, r1 = np.abs(T0[0][refl]).max(), np.abs(T1[0][refl]).max()
+    assert r0 > 0.05 * np.abs(T0[0][direct]).max()      # the rigid frame reflects
+    assert r1 < 0.1 * r0, (r0, r1)
