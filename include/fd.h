@@ -115,6 +115,18 @@ enum { FD_PEER_BLOB_BYTES = 512 };
 fd_status fd_peer_export(fd_ctx *ctx, void *blob, size_t cap, size_t *len);
 fd_status fd_peer_import(fd_ctx *ctx, const void *lo_blob, const void *hi_blob);
 
+/* Absorbing sponge frame (reading R#18 -- the paper is silent on
+ * boundaries, the band rule R#3 stays on the derivatives).  Cerjan et al. (1985):
+ * within `width` cells of each face, g(j) = exp(-(alpha (width - d))^2), d = min(j,
+ * n-1-j), G = g_z g_y g_x (fp64 per axis, rounded once to fp32), and each step is
+ *   P^{k+1} = G (2 P^k - G P^{k-1} + K S(P^k))        (fp32: G*((2p - G*pp) fma K S))
+ * on the stored fields -- Cerjan's damp-both-levels-after-the-step, so
+ * fd_get_wavefield(PREV) is the stored level (Cerjan's is G * PREV).  width 0 (the
+ * default) disables it; G = 1 keeps every kernel bitwise on the band-rule path.
+ * Classic values: width 20, alpha 0.015.  Before the first fd_step.
+ * Errors: FD_ERR_ARG (width < 0, alpha < 0 or not finite), FD_ERR_STATE. */
+fd_status fd_set_sponge(fd_ctx *ctx, int width, double alpha);
+
 /* Register a point source (add_source; R#4, R#5): before the stencil of step k,
  * P[idx] += amp * R(k dt) with the Ricker wavelet R(t) = (1 - 2 pi^2 f^2 (t-t0)^2)
  * exp(-pi^2 f^2 (t-t0)^2), evaluated in fp64 and rounded once to fp32.

@@ -11,5 +11,5 @@ from .fd import (  # noqa: F401
     FD_OPT_TSTEPS, FD_PEER_BLOB_BYTES, fd_peer_export, fd_peer_import,
     FD_OPT_VSLABS, FD_OPT_ZCHUNKS, FDError, Simulation, fd_add_source, fd_create, fd_create_dist, fd_destroy,
     fd_get_info, fd_get_kernel_times, fd_get_traces, fd_get_wavefield, fd_nccl_get_unique_id, fd_partition,
-    fd_set_option, fd_set_receivers, fd_set_stream, fd_set_wavefield, fd_step, lib,
+    fd_set_option, fd_set_receivers, fd_set_sponge, fd_set_stream, fd_set_wavefield, fd_step, lib,
 )

@@ -101,12 +101,54 @@ struct StepParams {
     float *traces;          // step-major [k][nrec_total]
     int32_t nrec_total;
     PeerPush peer1, peer2;  // in-kernel halo pushes of pnext / pnext2 (boundary launches)
+    const float *gsp;       // sponge frame (R#18): g_x[nx], g_y[ny], g_z[nzg] (global z); null = off
 };
 
+// Absorbing sponge frame (FD_OPT via fd_set_sponge; reading R#18, Cerjan 1985):
+// G = (g_z * g_y) * g_x at the point (indices clamped into the grid: two-step
+// stage A also evaluates ring points outside it, whose values are never used),
+// and the stored-field update P^{k+1} = G (2 P^k - G P^{k-1} + K S).  With
+// G = 1 it is bitwise the canonical fma(K, S, fma(2, p, -p_prev)).
+__device__ __forceinline__ float sponge_g(const StepParams &p, int gz, int y, int x) {
+    const int nx = (int)p.nx, ny = (int)p.ny, nzg = (int)p.nzg;
+    x = min(max(x, 0), nx - 1);
+    y = min(max(y, 0), ny - 1);
+    gz = min(max(gz, 0), nzg - 1);
+    return __fmul_rn(__fmul_rn(__ldg(p.gsp + nx + ny + gz), __ldg(p.gsp + nx + y)), __ldg(p.gsp + x));
+}
+// SP: the kernel instantiation with the frame (the tiled kernels are compiled
+// both ways so the band-rule path carries no sponge code); the reference
+// kernels test p.gsp at run time (time_update_rt).
+template <bool SP>
+__device__ __forceinline__ float time_update(const StepParams &p, float K, float S, float pc, float pp, int gz,
+                                             int y, int x) {
+    if constexpr (!SP) {
+        return __fmaf_rn(K, S, __fmaf_rn(2.f, pc, -pp));
+    } else {
+        const float G = sponge_g(p, gz, y, x);
+        return __fmul_rn(G, __fmaf_rn(K, S, __fmaf_rn(2.f, pc, -__fmul_rn(G, pp))));
+    }
+}
+__device__ __forceinline__ float time_update_rt(const StepParams &p, float K, float S, float pc, float pp, int gz,
+                                                int y, int x) {
+    return p.gsp ? time_update<true>(p, K, S, pc, pp, gz, y, x) : time_update<false>(p, K, S, pc, pp, gz, y, x);
+}
+
 // `off` = offset of the float4 within its plane (y * pitch + x), `plane` = ny * pitch
+// True when plane z of this slab is one of the planes pushed to a neighbour.
+// The tiled kernels take PEER as a template parameter: only boundary launches
+// of the peer transport run the PEER = true instantiation, so the push code
+// costs the other launches nothing.
+__device__ __forceinline__ bool peer_plane(const PeerPush &pp, int z, int nz) {
+    return (pp.lo && z < pp.push) || (pp.hi && z >= nz - pp.push);
+}
+
 template <int R>
 __device__ __forceinline__ void peer_store4(const PeerPush &pp, int z, int nz, int64_t plane, int64_t off,
                                             const float4 &v) {
+#ifdef FD_NO_PEER
+    return;
+#endif
     if (pp.lo && z < pp.push) *reinterpret_cast<float4 *>(pp.lo + (int64_t)(z + pp.lo_z) * plane + off) = v;
     if (pp.hi && z >= nz - pp.push)
         *reinterpret_cast<float4 *>(pp.hi + (int64_t)(z - nz + halo_planes(R)) * plane + off) = v;
@@ -273,7 +315,7 @@ struct Cfg {
 // grid = ntx * nty * nchunks CTAs; CTA b handles tile (b % ntiles) of z-chunk
 // (b / ntiles) (chunk-major, so co-resident CTAs stream the same z region and
 // share x-y halos in L2).  Warp NWC is the TMA producer; warps 0..NWC-1 compute.
-template <class C>
+template <class C, bool SP, bool PEER>
 __global__ void __launch_bounds__(C::NTHREADS)
 fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, BY, 1)
                   const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, TY, 1)
@@ -446,7 +488,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                     szz = __fmaf_rn(tap(R, m),
                                     __fadd_rn(f4(q[(PH + R - m) % Q][yy], e), f4(q[(PH + R + m) % Q][yy], e)), szz);
                 S = inz ? __fadd_rn(S, szz) : S;
-                const float upd = __fmaf_rn(f4(kk4, e), S, __fmaf_rn(2.f, pc, -f4(pp4, e)));
+                const float upd = time_update<SP>(prm, f4(kk4, e), S, pc, f4(pp4, e), gz, yb + yy, xb + e);
                 f4set(out[yy], e, upd);
             }
         }
@@ -487,11 +529,14 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             float *dst = prm.pnext + ((int64_t)(z + halo_planes(R)) * ny + yb) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
-                if (yb + yy < ny) {
-                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
-                    peer_store4<R>(prm.peer1, z, (int)prm.nz, (int64_t)ny * prm.pitch,
-                                   (int64_t)(yb + yy) * prm.pitch + xb, out[yy]);
-                }
+                if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+            if (PEER && peer_plane(prm.peer1, z, (int)prm.nz)) {
+#pragma unroll
+                for (int yy = 0; yy < C::NY; ++yy)
+                    if (yb + yy < ny)
+                        peer_store4<R>(prm.peer1, z, (int)prm.nz, (int64_t)ny * prm.pitch,
+                                       (int64_t)(yb + yy) * prm.pitch + xb, out[yy]);
+            }
         }
     };
     if constexpr (Q <= 5) {
@@ -539,7 +584,7 @@ struct Cfg2 {
     static_assert(TX % 4 == 0 && TY % NY == 0 && NCONS % 32 == 0, "tile");
 };
 
-template <class C>
+template <class C, bool SP, bool PEER>
 __global__ void __launch_bounds__(C::NTHREADS)
 tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, 1, BZ)
                    const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, 1, TY)
@@ -632,7 +677,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
                 for (int m = 1; m <= R; ++m)
                     sz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), sz);
                 S = inz ? __fadd_rn(S, sz) : S;
-                f4set(out[yy], e, __fmaf_rn(f4(kk4, e), S, __fmaf_rn(2.f, pc, -f4(pp4, e))));
+                f4set(out[yy], e, time_update<SP>(prm, f4(kk4, e), S, pc, f4(pp4, e), gz, 0, xb + e));
             }
         }
         __syncwarp();
@@ -669,10 +714,12 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             float *dst = prm.pnext + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
-                if (zt + yy < prm.zhi) {
-                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
-                    peer_store4<R>(prm.peer1, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
-                }
+                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+            if (PEER) {
+#pragma unroll
+                for (int yy = 0; yy < C::NY; ++yy)
+                    if (zt + yy < prm.zhi) peer_store4<R>(prm.peer1, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
+            }
         }
     }
 }
@@ -719,7 +766,7 @@ __global__ void naive_step_kernel(const StepParams prm) {
             S = __fadd_rn(S, s);
         }
         const int64_t ik = (z * ny + y) * P + x;
-        prm.pnext[i] = __fmaf_rn(prm.K[ik], S, __fmaf_rn(2.f, pc, -prm.pnext[i]));
+        prm.pnext[i] = time_update_rt(prm, prm.K[ik], S, pc, prm.pnext[i], (int)gz, (int)y, (int)x);
     }
 }
 
@@ -766,7 +813,7 @@ __global__ void time_update_kernel(const StepParams prm, const float *__restrict
         float S = pxx[ik];
         if (NDIM == 3) S = __fadd_rn(S, pyy[ik]);
         S = __fadd_rn(S, pzz[ik]);
-        prm.pnext[i] = __fmaf_rn(prm.K[ik], S, __fmaf_rn(2.f, prm.p[i], -prm.pnext[i]));
+        prm.pnext[i] = time_update_rt(prm, prm.K[ik], S, prm.p[i], prm.pnext[i], (int)(prm.gz0 + z), (int)y, (int)x);
     }
 }
 

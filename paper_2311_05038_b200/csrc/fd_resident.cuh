@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const StepParams prm,
                 S = __fadd_rn(S, sz);
             }
             float *const qq = Qr + (z + R) * PS + i;
-            const float v = __fmaf_rn(Ks[z * PS + i], S, __fmaf_rn(2.f, pc, -qq[0]));
+            const float v = time_update_rt(prm, Ks[z * PS + i], S, pc, qq[0], gz, p.y, p.x);
             qq[0] = v;
             if (z < R && qlo) qlo[(nplo + z + R) * PS + i] = v;
             if (z >= np - R && qhi) qhi[(z - np + R) * PS + i] = v;

@@ -103,57 +103,78 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t nx, int64_t ny, 
 typedef void (*launch_fused_t)(dim3, int, cudaStream_t, const CUtensorMap &, const CUtensorMap &,
                                const CUtensorMap &, const StepParams &);
 
+// Each tiled kernel is compiled in up to four variants v = SP | 2 * PEER:
+// bit 0 the sponge frame (R#18), bit 1 the in-kernel halo pushes of the peer
+// transport.  Tuning-only entries carry variant 0 alone; the configurations
+// the auto policy picks ("full") carry all four.
 struct TileCfg {
     int ndim, r, tx, ty, ny, dp, dk;
     int pbw, tbw;        // TMA box widths (halo'd p row piece, p_prev/K row piece)
     int pbz, tbz;        // TMA box depths in z (2D row blocks; 1 in 3D)
     int threads, smem;
-    const void *kernel;
-    launch_fused_t launch;
+    const void *kernel[4];
+    launch_fused_t launch[4];
+    bool full() const { return kernel[3] != nullptr; }
 };
 
-template <class C>
-static void launch_fused(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
-                         const CUtensorMap &c, const StepParams &p) {
-    fused_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
-}
+#define FD_LAUNCHER(NAME, KERNEL)                                                                            \
+    template <class C, int V>                                                                                \
+    static void NAME(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,       \
+                     const CUtensorMap &c, const StepParams &p) {                                            \
+        KERNEL<C, (V & 1) != 0, (V & 2) != 0><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);                \
+    }
+FD_LAUNCHER(launch_fused, fused_step_kernel)
+FD_LAUNCHER(launch_tile2d, tile2d_step_kernel)
+FD_LAUNCHER(launch_tb2ws, tb2ws_step_kernel)
+FD_LAUNCHER(launch_tb2d, tb2d_step_kernel)
 
-template <int R, int NDIM, int TX, int TY, int NY, int DP, int DK>
+#define FD_VARIANTS(T, C, FULL, KERNEL, LAUNCH)                                                              \
+    do {                                                                                                     \
+        T.kernel[0] = (const void *)KERNEL<C, false, false>;                                                  \
+        T.launch[0] = LAUNCH<C, 0>;                                                                          \
+        if constexpr (FULL) {                                                                                \
+            T.kernel[1] = (const void *)KERNEL<C, true, false>;                                               \
+            T.kernel[2] = (const void *)KERNEL<C, false, true>;                                               \
+            T.kernel[3] = (const void *)KERNEL<C, true, true>;                                                \
+            T.launch[1] = LAUNCH<C, 1>;                                                                      \
+            T.launch[2] = LAUNCH<C, 2>;                                                                      \
+            T.launch[3] = LAUNCH<C, 3>;                                                                      \
+        }                                                                                                    \
+    } while (0)
+
+template <int R, int NDIM, int TX, int TY, int NY, int DP, int DK, bool FULL = false>
 static TileCfg make_cfg() {
     using C = Cfg<R, NDIM, TX, TY, NY, DP, DK>;
-    return TileCfg{NDIM, R, TX, TY, NY, DP, DK, C::PBW, C::TBW, 1, 1, C::NTHREADS, C::SMEM_BYTES,
-                   (const void *)fused_step_kernel<C>, launch_fused<C>};
+    TileCfg t{NDIM, R, TX, TY, NY, DP, DK, C::PBW, C::TBW, 1, 1, C::NTHREADS, C::SMEM_BYTES, {}, {}};
+    FD_VARIANTS(t, C, FULL, fused_step_kernel, launch_fused);
+    return t;
 }
 
-template <class C>
-static void launch_tile2d(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
-                          const CUtensorMap &c, const StepParams &p) {
-    tile2d_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
-}
-
-template <int R, int TX, int TY, int NY, int NS>
+template <int R, int TX, int TY, int NY, int NS, bool FULL = false>
 static TileCfg make_cfg2() {
     using C = Cfg2<R, TX, TY, NY, NS>;
-    return TileCfg{2, R, TX, TY, NY, NS, 0, C::PBW, C::TBW, C::PBZ, C::TBZ, C::NTHREADS, C::SMEM_BYTES,
-                   (const void *)tile2d_step_kernel<C>, launch_tile2d<C>};
+    TileCfg t{2, R, TX, TY, NY, NS, 0, C::PBW, C::TBW, C::PBZ, C::TBZ, C::NTHREADS, C::SMEM_BYTES, {}, {}};
+    FD_VARIANTS(t, C, FULL, tile2d_step_kernel, launch_tile2d);
+    return t;
 }
 
 // Compiled tiles (index = position in this table; FD_OPT_TILE selects one).
 // 3D (fused_step_kernel): x-y tiles with rows per thread NY (4 for r <= 2, 2
 // or 1 above, to bound the register queue), p-ring prefetch DP, (p_prev, K)
 // ring prefetch DK.  2D (tile2d_step_kernel): TX columns x TY-row blocks, NS
-// ring slots.  scripts/tune.py sweeps them; choose_tile() encodes the result.
-#define CFG3(R, NY) make_cfg<R, 3, 64, 32, NY, 2, 2>(), make_cfg<R, 3, 128, 32, NY, 2, 2>(), \
-                    make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2>(), \
+// ring slots.  scripts/tune.py sweeps them; choose_tile() encodes the result
+// (the preferred entry per (ndim, r) is the "full" one).
+#define CFG3(R, NY, F1, F2) make_cfg<R, 3, 64, 32, NY, 2, 2>(), make_cfg<R, 3, 128, 32, NY, 2, 2, F2>(), \
+                    make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2, F1>(), \
                     make_cfg<R, 3, 64, 32, NY, 1, 1>(), make_cfg<R, 3, 32, 32, NY, 2, 2>()
 #define CFG3W(R) make_cfg<R, 3, 64, 32, 2, 2, 2>(), make_cfg<R, 3, 32, 32, 2, 2, 2>(), \
-                 make_cfg<R, 3, 64, 16, 2, 2, 2>(), make_cfg<R, 3, 128, 16, 2, 2, 2>(), \
+                 make_cfg<R, 3, 64, 16, 2, 2, 2, true>(), make_cfg<R, 3, 128, 16, 2, 2, 2>(), \
                  make_cfg<R, 3, 64, 16, 1, 2, 2>(), make_cfg<R, 3, 64, 16, 2, 1, 1>()
 #define CFG2(R) make_cfg2<R, 128, 32, 4, 3>(), make_cfg2<R, 128, 16, 4, 4>(), \
                 make_cfg2<R, 64, 32, 4, 4>(), make_cfg2<R, 128, 64, 8, 2>(), \
-                make_cfg2<R, 64, 16, 2, 4>(), make_cfg2<R, 64, 32, 4, 3>(), make_cfg2<R, 64, 32, 2, 3>()
+                make_cfg2<R, 64, 16, 2, 4>(), make_cfg2<R, 64, 32, 4, 3, true>(), make_cfg2<R, 64, 32, 2, 3>()
 static const std::vector<TileCfg> &tile_table() {
-    static const std::vector<TileCfg> t = {CFG3(1, 4), CFG3(2, 4), CFG3W(3), CFG3W(4),
+    static const std::vector<TileCfg> t = {CFG3(1, 4, true, false), CFG3(2, 4, false, true), CFG3W(3), CFG3W(4),
                                            CFG2(1),    CFG2(2),    CFG2(3),    CFG2(4)};
     return t;
 }
@@ -162,27 +183,19 @@ static const std::vector<TileCfg> &tile_table() {
 // Two-steps-per-pass (temporal blocking) tiles, 3D, r <= 2 (fd_tb2.cuh).
 // Presented as TileCfg so the chunking/receiver code is shared: pbw/pbz hold
 // the P^k box (BX0, BY0), tbw/tbz the grown-tile box (BXE, BYE).
-template <class C>
-static void launch_tb2ws(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
-                         const CUtensorMap &c, const StepParams &p) {
-    tb2ws_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
-}
-template <int R, int TX, int TY, int NYA, int NYB, int DP, int DA, int D1, int MINB = 1>
+template <int R, int TX, int TY, int NYA, int NYB, int DP, int DA, int D1, int MINB = 1, bool FULL = false>
 static TileCfg make_tb2ws() {
     using C = CfgWS<R, TX, TY, NYA, NYB, DP, DA, D1, MINB>;
-    return TileCfg{3, R, TX, TY, NYB, DP, DA, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES,
-                   (const void *)tb2ws_step_kernel<C>, launch_tb2ws<C>};
+    TileCfg t{3, R, TX, TY, NYB, DP, DA, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
+    FD_VARIANTS(t, C, FULL, tb2ws_step_kernel, launch_tb2ws);
+    return t;
 }
-template <class C>
-static void launch_tb2d(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
-                        const CUtensorMap &c, const StepParams &p) {
-    tb2d_step_kernel<C><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);
-}
-template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1>
+template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1, bool FULL = false>
 static TileCfg make_tb2d() {
     using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB>;
-    return TileCfg{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES,
-                   (const void *)tb2d_step_kernel<C>, launch_tb2d<C>};
+    TileCfg t{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
+    FD_VARIANTS(t, C, FULL, tb2d_step_kernel, launch_tb2d);
+    return t;
 }
 
 static const std::vector<TileCfg> &tb2_table() {
@@ -192,21 +205,21 @@ static const std::vector<TileCfg> &tb2_table() {
         // the r03 choice (64 x 16, two CTAs per SM, 5/4 slots) 518; 64 x 16 with
         // 6/5 slots 542; 128 x 16 with 5/4 slots 534; more stage-B warps
         // (NYB = 2) 481-551
-        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1>(),
+        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1, true>(), make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1>(),
         make_tb2ws<1, 128, 16, 2, 4, 3, 3, 3, 1>(), make_tb2ws<1, 64, 16, 2, 4, 3, 3, 1, 2>(),
         make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
         // 3D r=2 (order 4 stays on single steps by default: 421 vs <= 320 Gpts/s in r03)
-        make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
+        make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1, 1, true>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
         make_tb2ws<2, 64, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<2, 128, 8, 2, 2, 3, 3, 2, 1>(),
         make_tb2ws<2, 64, 16, 2, 4, 2, 2, 2, 1>(),
         // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows.  r04 sweep
         // (C2): order 2 554 Gpts/s (3 stages, two CTAs per SM; 518 with 2) vs
         // 400 single-step; order 4 486 vs 397; order 6 391 vs 392; order 8 328 vs 385
-        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
+        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2, true>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
         make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
-        make_tb2d<2, 64, 28, 4, 4, 3, 2>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
-        make_tb2d<3, 64, 26, 4, 2, 3, 2>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
-        make_tb2d<4, 64, 24, 4, 4, 3, 2>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
+        make_tb2d<2, 64, 28, 4, 4, 3, 2, 1, true>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
+        make_tb2d<3, 64, 26, 4, 2, 3, 2, 1, true>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
+        make_tb2d<4, 64, 24, 4, 4, 3, 2, 1, true>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
         make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>()};
     return t;
 }
@@ -352,6 +365,10 @@ struct fd_ctx {
     bool frozen = false;                  // fd_peer_export done: options fixed
     int64_t *d_flags = nullptr;           // [0]: written by rank - 1, [1]: by rank + 1 (exchange counts)
     int64_t xcount = 0;                   // exchanges this rank has signalled
+    // absorbing sponge frame (fd_set_sponge, R#18)
+    int sponge_nb = 0;
+    double sponge_alpha = 0;
+    float *d_gsp = nullptr;               // g_x[nx], g_y[ny], g_z[nzg] (fp64 profile rounded once)
     bool overlap = false;                 // boundary/interior split on two streams
     int tile = -1, occ = 0, nsm = 148;
     // FD_OPT_PROFILE: CUDA events around every launch, folded into per-kernel sums
@@ -418,6 +435,8 @@ static void destroy_all(fd_ctx *c) {
     dev_free(c->d_wtab);
     dev_free(c->d_k);
     dev_free(c->d_res_rec);
+    dev_free(c->d_gsp);
+    c->d_gsp = nullptr;
     for (auto *pr : {&c->plo, &c->phi})
         for (void *m : pr->opened) cudaIpcCloseMemHandle(m);
     c->plo.opened.clear(); c->phi.opened.clear();
@@ -574,14 +593,20 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
 }
 
 // ------------------------------------------------------------ kernel choice
+// Resident CTAs per SM of a configuration: the minimum over its compiled variants.
 static int occupancy(const TileCfg &t) {
-    int n = 0;
-    cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.kernel, t.threads, t.smem) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
+    int best = -1;
+    for (int v = 0; v < 4; ++v) {
+        if (!t.kernel[v]) continue;
+        int n = 0;
+        cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.kernel[v], t.threads, t.smem) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        best = best < 0 ? n : std::min(best, n);
     }
-    return n;
+    return std::max(best, 0);
 }
 
 static int64_t ntiles_of(const fd_ctx *c, const TileCfg &t) {
@@ -632,6 +657,10 @@ static bool preferred(const fd_ctx *c, const TileCfg &t) {
     return t.tx == 64 && t.ty == 32 && t.ny == 4 && t.dp == 3;
 }
 
+// The sponge frame and the peer transport run the kernel variants compiled
+// for the "full" table entries only.
+static bool needs_full(const fd_ctx *c) { return c->sponge_nb > 0 || c->opt_transport == 1; }
+
 static void choose_tile(fd_ctx *c, int64_t span) {
     (void)span;
     const auto &tab = tile_table();
@@ -641,6 +670,7 @@ static void choose_tile(fd_ctx *c, int64_t span) {
             const TileCfg &t = tab[i];
             if (t.ndim != c->ndim || t.r != c->R) continue;
             if (c->opt_tile >= 0 ? i != c->opt_tile : (pass == 0 && !preferred(c, t))) continue;
+            if (needs_full(c) && !t.full()) continue;   // sponge / peer variants compiled for full entries
             const int occ = occupancy(t);
             if (occ <= 0) continue;
             bi = i; bocc = occ;
@@ -868,6 +898,24 @@ static fd_status prepare(fd_ctx *c) {
     }
     c->d_k = (int64_t *)dev_alloc(sizeof(int64_t));
     if (!c->d_k) return fail(FD_ERR_NOMEM, "step counter allocation failed");
+    if (c->sponge_nb > 0) {
+        // Cerjan profile per axis (R#18), fp64 rounded once: g = exp(-(alpha (nb - d))^2)
+        // for d = min(j, n-1-j) < nb, else 1; z over the GLOBAL planes
+        std::vector<float> h;
+        auto axis = [&](int64_t n) {
+            for (int64_t j = 0; j < n; ++j) {
+                const int64_t d = std::min(j, n - 1 - j);
+                const double a = c->sponge_alpha * (double)(c->sponge_nb - d);
+                h.push_back(d < c->sponge_nb ? (float)std::exp(-(a * a)) : 1.0f);
+            }
+        };
+        axis(c->nxg);
+        if (c->ndim == 3) axis(c->nyg); else h.push_back(1.0f);
+        axis(c->nzg);
+        c->d_gsp = (float *)dev_alloc(h.size() * 4);
+        if (!c->d_gsp) return fail(FD_ERR_NOMEM, "sponge table allocation failed");
+        CUDA_TRY(c, cudaMemcpy(c->d_gsp, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    }
     if (c->opt_resident != 1 && c->opt_kernel == 0) {
         // auto: small single-slab grids with no pinned tile / step mode
         const bool want = c->opt_resident == 2 ||
@@ -892,7 +940,9 @@ static fd_status prepare(fd_ctx *c) {
         choose_tile(c, maxnz);
         if (c->tile < 0) return fail(FD_ERR_CUDA, "no fused kernel configuration fits this device");
         const TileCfg &t = tile_table()[c->tile];
-        CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
+        for (int v = 0; v < 4; ++v)
+            if (t.kernel[v])
+                CUDA_TRY(c, cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
     }
     if (c->opt_tsteps == 0) {
         // auto: temporal blocking where it is faster (r04 sweeps: 3D order 2
@@ -945,12 +995,15 @@ static fd_status prepare(fd_ctx *c) {
         const auto &tb = tb2_table();
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
             if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
+            if (needs_full(c) && !tb[i].full()) continue;
             const int occ = occupancy(tb[i]);
             if (occ > 0) { c->tb2 = i; c->tb2occ = occ; }
         }
         if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
         const TileCfg &t = tb[c->tb2];
-        CUDA_TRY(c, cudaFuncSetAttribute(t.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
+        for (int v = 0; v < 4; ++v)
+            if (t.kernel[v])
+                CUDA_TRY(c, cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
         const TileCfg &ts = tile_table()[c->tile];
         for (auto &s : c->slabs) {
             const size_t fbytes = (size_t)buf_floats(c, s) * 4;
@@ -1074,6 +1127,7 @@ static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepPar
     }
     p.traces = c->d_traces;
     p.nrec_total = (int32_t)c->rec.size();
+    p.gsp = c->d_gsp;
     // step index: baked (plain launches) or *d_k + offset (graph capture)
     p.k = step_k;
     if (c->capturing) { p.kdev = c->d_k; p.koff = (int32_t)(step_k - c->gk0); }
@@ -1224,8 +1278,10 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     g.ctas = (int)grid.x;
     const CUtensorMap &mp = s.mHalo[c->icur];
     const CUtensorMap &mpp = s.mTile[c->iprev];
-    if (c->opt_transport == 1 && g.boundary) set_push(c, s, p, c->iprev, c->opt_tsteps == 2 ? c->H : c->R, -1, 0);
-    tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, mp, mpp, s.mK, p); });
+    const bool push = c->opt_transport == 1 && g.boundary;
+    if (push) set_push(c, s, p, c->iprev, c->opt_tsteps == 2 ? c->H : c->R, -1, 0);
+    const launch_fused_t go = t.launch[(c->d_gsp ? 1 : 0) | (push ? 2 : 0)];
+    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
 // Halo exchange of `depth` planes per face of field buffer b (b = -1: K).
@@ -1414,8 +1470,10 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
-    if (c->opt_transport == 1 && g.boundary) set_push(c, s, p, f1, c->R, f2, c->H);
-    tracked(c, FD_K_FUSED, st, [&] { t.launch(grid, t.smem, st, m0, mm, s.mKe, p); });
+    const bool push = c->opt_transport == 1 && g.boundary;
+    if (push) set_push(c, s, p, f1, c->R, f2, c->H);
+    const launch_fused_t go = t.launch[(c->d_gsp ? 1 : 0) | (push ? 2 : 0)];
+    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, m0, mm, s.mKe, p); });
 }
 
 static fd_status two_steps(fd_ctx *c) {
@@ -1587,6 +1645,16 @@ static fd_status check_index(fd_ctx *c, const int64_t *idx, int64_t g[3]) {
     if (g[0] < 0 || g[0] >= c->nzg || g[1] < 0 || g[1] >= c->nyg || g[2] < 0 || g[2] >= c->nxg)
         return fail(FD_ERR_RANGE, "index (%lld, %lld, %lld) outside the grid", (long long)g[0], (long long)g[1],
                     (long long)g[2]);
+    return FD_OK;
+}
+
+fd_status fd_set_sponge(fd_ctx *c, int width, double alpha) {
+    fd_status s = check_ctx(c);
+    if (s) return s;
+    if (width < 0 || !(alpha >= 0) || !std::isfinite(alpha)) return fail(FD_ERR_ARG, "width >= 0, alpha >= 0 finite");
+    if (c->started || c->frozen) return fail(FD_ERR_STATE, "fd_set_sponge only before the first fd_step");
+    c->sponge_nb = width;
+    c->sponge_alpha = alpha;
     return FD_OK;
 }
 

@@ -60,7 +60,7 @@ struct CfgWS {
     static_assert(BX0 <= 256 && BY0 <= 256 && R <= 4, "TMA box");
 };
 
-template <class C>
+template <class C, bool SP, bool PEER>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant__ CUtensorMap map_pm,
                   const __grid_constant__ CUtensorMap map_k, const StepParams prm) {
@@ -176,6 +176,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             const int gz = (int)prm.gz0 + z1;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
             const bool store = (z1 >= z0) && (z1 < z1e);
+            const bool push1 = PEER && peer_plane(prm.peer1, z1, (int)prm.nz);
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -210,7 +211,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         for (int m = 1; m <= R; ++m)
                             szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
                         S = inz ? __fadd_rn(S, szz) : S;
-                        f4set(o, e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pm4, e))));
+                        f4set(o, e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pm4, e), gz, y, xb + e));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && y < ny;
                     oraw[yy] = o;
@@ -224,7 +225,9 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
                     if (store && interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + halo_planes(R)) * ny + y) * prm.pitch + xb) = o;
-                        peer_store4<R>(prm.peer1, z1, (int)prm.nz, (int64_t)ny * prm.pitch, (int64_t)y * prm.pitch + xb, o);
+                        if (push1)
+                            peer_store4<R>(prm.peer1, z1, (int)prm.nz, (int64_t)ny * prm.pitch,
+                                           (int64_t)y * prm.pitch + xb, o);
                     }
                 }
             }
@@ -333,7 +336,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     for (int m = 1; m <= R; ++m)
                         szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
                     S = inz ? __fadd_rn(S, szz) : S;
-                    f4set(out[yy], e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pk4, e))));
+                    f4set(out[yy], e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pk4, e), gz, y, xb + e));
                 }
             }
         }
@@ -373,11 +376,14 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float *dst = prm.pnext2 + ((int64_t)(z2 + halo_planes(R)) * ny + y0 + ri0) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
-                if (y0 + ri0 + yy < ny) {
-                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
-                    peer_store4<R>(prm.peer2, z2, (int)prm.nz, (int64_t)ny * prm.pitch,
-                                   (int64_t)(y0 + ri0 + yy) * prm.pitch + xb, out[yy]);
-                }
+                if (y0 + ri0 + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+            if (PEER && peer_plane(prm.peer2, z2, (int)prm.nz)) {
+#pragma unroll
+                for (int yy = 0; yy < C::NYB; ++yy)
+                    if (y0 + ri0 + yy < ny)
+                        peer_store4<R>(prm.peer2, z2, (int)prm.nz, (int64_t)ny * prm.pitch,
+                                       (int64_t)(y0 + ri0 + yy) * prm.pitch + xb, out[yy]);
+            }
         }
     }
 }
@@ -410,7 +416,7 @@ struct CfgWS2 {
     static_assert(BX0 <= 256 && BY0 <= 256 && R <= 4, "TMA box");
 };
 
-template <class C>
+template <class C, bool SP, bool PEER>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box (BX0, 1, BY0)
                  const __grid_constant__ CUtensorMap map_pm,   // P^{k-1} buffer, box (BXE, 1, BYE)
@@ -423,6 +429,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     uint64_t *bars = reinterpret_cast<uint64_t *>(sP1 + C::N1 * C::EF);
     uint64_t *fullS = bars, *emptyS = fullS + C::NS, *full1 = emptyS + C::NS, *empty1 = full1 + C::N1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr bool anyp = PEER;                          // in-kernel halo pushes (boundary launches)
     const int unit = blockIdx.x;
     const int chunk = unit / prm.ntx;
     const int x0 = (unit - chunk * prm.ntx) * C::TX;
@@ -511,7 +518,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         for (int m = 1; m <= R; ++m)
                             szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
                         S = inz ? __fadd_rn(S, szz) : S;
-                        f4set(o, e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pm4, e))));
+                        f4set(o, e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pm4, e), gz, 0, xb + e));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && z < prm.zhi;
                     oraw[yy] = o;
@@ -525,7 +532,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
                     if (interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + halo_planes(R)) * prm.pitch + xb) = o;
-                        peer_store4<R>(prm.peer1, z, (int)prm.nz, prm.pitch, xb, o);
+                        if (anyp) peer_store4<R>(prm.peer1, z, (int)prm.nz, prm.pitch, xb, o);
                     }
                 }
             }
@@ -589,7 +596,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     for (int m = 1; m <= R; ++m)
                         szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
                     S = inz ? __fadd_rn(S, szz) : S;
-                    f4set(out[yy], e, __fmaf_rn(f4(k4, e), S, __fmaf_rn(2.f, pc, -f4(pk4, e))));
+                    f4set(out[yy], e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pk4, e), gz, 0, xb + e));
                 }
             }
         }
@@ -622,10 +629,13 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             float *dst = prm.pnext2 + (int64_t)(zt + halo_planes(R)) * prm.pitch + xb;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
-                if (zt + yy < prm.zhi) {
-                    *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
-                    peer_store4<R>(prm.peer2, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
-                }
+                if (zt + yy < prm.zhi) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+            if (PEER) {
+#pragma unroll
+                for (int yy = 0; yy < C::NYB; ++yy)
+                    if (zt + yy < prm.zhi)
+                        peer_store4<R>(prm.peer2, zt + yy, (int)prm.nz, prm.pitch, xb, out[yy]);
+            }
         }
     }
 }

@@ -33,7 +33,7 @@ EXPORTED = [
     "fd_set_receivers", "fd_step", "fd_get_wavefield", "fd_get_traces", "fd_destroy",
     "fd_strerror", "fd_last_error", "fd_set_stream", "fd_set_allocator", "fd_set_wavefield",
     "fd_set_option", "fd_get_info", "fd_get_kernel_times", "fd_reset_kernel_times",
-    "fd_peer_export", "fd_peer_import",
+    "fd_peer_export", "fd_peer_import", "fd_set_sponge",
 ]
 
 
@@ -103,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "fd_reset_kernel_times": ([ctypes.c_void_p], st),
         "fd_peer_export": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], st),
         "fd_peer_import": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], st),
+        "fd_set_sponge": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_double], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -180,6 +181,10 @@ def fd_peer_import(ctx, lo_blob: bytes | None, hi_blob: bytes | None):
     lo = ctypes.create_string_buffer(lo_blob, len(lo_blob)) if lo_blob else None
     hi = ctypes.create_string_buffer(hi_blob, len(hi_blob)) if hi_blob else None
     _check(lib.fd_peer_import(ctx, lo, hi), "fd_peer_import")
+
+
+def fd_set_sponge(ctx, width: int, alpha: float = 0.015):
+    _check(lib.fd_set_sponge(ctx, int(width), float(alpha)), "fd_set_sponge")
 
 
 def fd_add_source(ctx, idx, f_peak_hz: float, t0_s: float, amp: float = 1.0):
@@ -302,6 +307,10 @@ class Simulation:
 
     def add_source(self, idx, f, t0, amp=1.0):
         fd_add_source(self.ctx, idx, f, t0, amp)
+
+    def set_sponge(self, width: int, alpha: float = 0.015):
+        """Absorbing Cerjan frame (fd_set_sponge; reading R#18)."""
+        fd_set_sponge(self.ctx, width, alpha)
 
     def set_receivers(self, idx):
         idx = np.asarray(idx, dtype=np.int64).reshape(-1, len(self.global_dims))
