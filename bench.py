@@ -251,7 +251,7 @@ def _velocity(wl, world):
     return velocity(wl.model, gdims, z0, z1), gdims
 
 
-def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl"):
+def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl", sponge=0):
     """This rank's simulation: the whole grid at N=1; at N>1 a z-slab of the
     weak-scaled grid (N copies of the workload's grid stacked along z,
     slab-decomposed, halo exchange inside libfd.so: NCCL send/recv, or the
@@ -263,6 +263,8 @@ def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl"
         from paper_2311_05038_b200 import dist as fdd
         sim = fdd.create(vel, gdims, wl.h, wl.dt, wl.order, device=dist_env()[2], stream=stream,
                          options=options, transport=transport)
+    if sponge:
+        sim.set_sponge(sponge, 0.015)        # Cerjan frame (R#18), classic alpha
     for s in wl.sources:
         sim.add_source(s.idx, s.f, s.t0, s.amp)
     sim.set_receivers(wl.receivers)
@@ -288,7 +290,8 @@ def run_ours(args, wl):
     if args.no_graph:
         opts[fd.FD_OPT_GRAPH] = 0
     opts[fd.FD_OPT_TSTEPS] = args.tsteps
-    sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport)
+    sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport,
+                    sponge=args.sponge)
     sim.step(args.warmup)
     # setup for the timed steps (trace/wavelet tables for both passes, the CUDA
     # graphs to replay) happens here, outside the timed region
@@ -347,7 +350,7 @@ def run_ours(args, wl):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        s2 = _make_sim(wl, world, vel_pin, gdims, transport=args.transport)
+        s2 = _make_sim(wl, world, vel_pin, gdims, transport=args.transport, sponge=args.sponge)
         s2.step(args.steps)
         T2 = s2.traces()
         W2 = s2.wavefield(out=out_pin)
@@ -411,6 +414,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
                    "parallelism": (f"z-slabs x{world} ({'in-kernel peer-store' if args.transport == 'peer' else 'NCCL'}"
                                    f" halo exchange)") if world > 1 else "1 GPU",
                    **({"shared_gpu": True} if os.environ.get("FD_BENCH_SHARE_GPU") == "1" else {}),
+                   **({"sponge_cells": args.sponge} if args.sponge else {}),
                    "global_grid": [wl.dims[0] * world] + list(wl.dims[1:]),
                    "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -436,6 +440,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="plain launches instead of CUDA-graph replay")
     ap.add_argument("--clock-sampler", default="nvml", choices=["nvml", "smi"])
+    ap.add_argument("--sponge", type=int, default=0,
+                    help="absorbing Cerjan frame of this many cells (fd_set_sponge, alpha 0.015); 0 = band rule only")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="halo transport at N>1: NCCL send/recv or in-kernel peer stores (CUDA IPC)")
     ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2],

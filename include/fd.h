@@ -118,8 +118,8 @@ fd_status fd_peer_import(fd_ctx *ctx, const void *lo_blob, const void *hi_blob);
 /* Absorbing sponge frame (reading R#18 -- the paper is silent on
  * boundaries, the band rule R#3 stays on the derivatives).  Cerjan et al. (1985):
  * within `width` cells of each face, g(j) = exp(-(alpha (width - d))^2), d = min(j,
- * n-1-j), G = g_z g_y g_x (fp64 per axis, rounded once to fp32), and each step is
- *   P^{k+1} = G (2 P^k - G P^{k-1} + K S(P^k))        (fp32: G*((2p - G*pp) fma K S))
+ * n-1-j), G = g_z (g_y g_x) (fp64 per axis, rounded once to fp32), and each step is
+ *   P^{k+1} = G (2 P^k - G P^{k-1} + K S(P^k))        (fp32: G * fma(K, S, fma(2, p, -(G pp))))
  * on the stored fields -- Cerjan's damp-both-levels-after-the-step, so
  * fd_get_wavefield(PREV) is the stored level (Cerjan's is G * PREV).  width 0 (the
  * default) disables it; G = 1 keeps every kernel bitwise on the band-rule path.

@@ -104,34 +104,40 @@ struct StepParams {
     const float *gsp;       // sponge frame (R#18): g_x[nx], g_y[ny], g_z[nzg] (global z); null = off
 };
 
-// Absorbing sponge frame (FD_OPT via fd_set_sponge; reading R#18, Cerjan 1985):
-// G = (g_z * g_y) * g_x at the point (indices clamped into the grid: two-step
-// stage A also evaluates ring points outside it, whose values are never used),
-// and the stored-field update P^{k+1} = G (2 P^k - G P^{k-1} + K S).  With
-// G = 1 it is bitwise the canonical fma(K, S, fma(2, p, -p_prev)).
-__device__ __forceinline__ float sponge_g(const StepParams &p, int gz, int y, int x) {
-    const int nx = (int)p.nx, ny = (int)p.ny, nzg = (int)p.nzg;
-    x = min(max(x, 0), nx - 1);
-    y = min(max(y, 0), ny - 1);
-    gz = min(max(gz, 0), nzg - 1);
-    return __fmul_rn(__fmul_rn(__ldg(p.gsp + nx + ny + gz), __ldg(p.gsp + nx + y)), __ldg(p.gsp + x));
+// Absorbing sponge frame (fd_set_sponge; reading R#18, Cerjan 1985).  The
+// per-axis factors come from the fp32 tables g_x, g_y, g_z (global z); indices
+// are clamped into the grid (two-step stage A also evaluates ring points
+// outside it, whose values are never used).  Canonical fp32 order:
+//   G = g_z * (g_y * g_x),   P^{k+1} = G * fma(K, S, fma(2, p, -(G * p_prev)))
+// With G = 1 this is bitwise the canonical fma(K, S, fma(2, p, -p_prev)).  The
+// tiled kernels hold a thread's g_x (its 4 x points) and g_y (its rows) in
+// registers and load g_z once per plane.
+__device__ __forceinline__ float sponge_axis(const StepParams &p, int off, int n, int i) {
+    return __ldg(p.gsp + off + min(max(i, 0), n - 1));
+}
+__device__ __forceinline__ float sponge_gx(const StepParams &p, int x) { return sponge_axis(p, 0, (int)p.nx, x); }
+__device__ __forceinline__ float sponge_gy(const StepParams &p, int y) {
+    return sponge_axis(p, (int)p.nx, (int)p.ny, y);
+}
+__device__ __forceinline__ float sponge_gz(const StepParams &p, int gz) {
+    return sponge_axis(p, (int)(p.nx + p.ny), (int)p.nzg, gz);
 }
 // SP: the kernel instantiation with the frame (the tiled kernels are compiled
 // both ways so the band-rule path carries no sponge code); the reference
 // kernels test p.gsp at run time (time_update_rt).
 template <bool SP>
-__device__ __forceinline__ float time_update(const StepParams &p, float K, float S, float pc, float pp, int gz,
-                                             int y, int x) {
+__device__ __forceinline__ float time_update(float K, float S, float pc, float pp, float gz, float gy, float gx) {
     if constexpr (!SP) {
         return __fmaf_rn(K, S, __fmaf_rn(2.f, pc, -pp));
     } else {
-        const float G = sponge_g(p, gz, y, x);
+        const float G = __fmul_rn(gz, __fmul_rn(gy, gx));
         return __fmul_rn(G, __fmaf_rn(K, S, __fmaf_rn(2.f, pc, -__fmul_rn(G, pp))));
     }
 }
 __device__ __forceinline__ float time_update_rt(const StepParams &p, float K, float S, float pc, float pp, int gz,
                                                 int y, int x) {
-    return p.gsp ? time_update<true>(p, K, S, pc, pp, gz, y, x) : time_update<false>(p, K, S, pc, pp, gz, y, x);
+    if (!p.gsp) return time_update<false>(K, S, pc, pp, 1.f, 1.f, 1.f);
+    return time_update<true>(K, S, pc, pp, sponge_gz(p, gz), sponge_gy(p, y), sponge_gx(p, x));
 }
 
 // `off` = offset of the float4 within its plane (y * pitch + x), `plane` = ny * pitch
@@ -398,6 +404,11 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     bool iny[C::NY];
 #pragma unroll
     for (int yy = 0; yy < C::NY; ++yy) iny[yy] = (C::NDIM == 3) && (yb + yy >= R) && (yb + yy < ny - R);
+    float sgx[4], sgy[C::NY];                     // sponge factors (SP only)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
+#pragma unroll
+    for (int yy = 0; yy < C::NY; ++yy) sgy[yy] = SP ? sponge_gy(prm, yb + yy) : 1.f;
 
     // sources that fall in this CTA's tile and chunk
     uint32_t smask = 0;
@@ -450,6 +461,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         const float *tk = sK + ks * C::K_FLOATS;
         const int gz = (int)prm.gz0 + z;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
+        const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
 
         float4 col[C::NY + 2 * C::HY];
         if (C::NDIM == 3) {
@@ -488,7 +500,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                     szz = __fmaf_rn(tap(R, m),
                                     __fadd_rn(f4(q[(PH + R - m) % Q][yy], e), f4(q[(PH + R + m) % Q][yy], e)), szz);
                 S = inz ? __fadd_rn(S, szz) : S;
-                const float upd = time_update<SP>(prm, f4(kk4, e), S, pc, f4(pp4, e), gz, yb + yy, xb + e);
+                const float upd = time_update<SP>(f4(kk4, e), S, pc, f4(pp4, e), sgz, sgy[yy], sgx[e]);
                 f4set(out[yy], e, upd);
             }
         }
@@ -633,6 +645,9 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    float sgx[4];                                 // sponge factors (SP only)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
     uint32_t smask = 0;
     const int zc0 = prm.zlo + b0 * C::TY, zc1 = min(prm.zhi, prm.zlo + b1 * C::TY);
     for (int q = 0; q < prm.nsrc; ++q)
@@ -665,6 +680,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
             const int gz = (int)prm.gz0 + zt + yy;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
+            const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float pc = a[4 + e];
@@ -677,7 +693,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
                 for (int m = 1; m <= R; ++m)
                     sz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), sz);
                 S = inz ? __fadd_rn(S, sz) : S;
-                f4set(out[yy], e, time_update<SP>(prm, f4(kk4, e), S, pc, f4(pp4, e), gz, 0, xb + e));
+                f4set(out[yy], e, time_update<SP>(f4(kk4, e), S, pc, f4(pp4, e), sgz, 1.f, sgx[e]));
             }
         }
         __syncwarp();

@@ -133,6 +133,11 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         bool inx[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+        float sgx[4], sgy[C::NYA];                     // sponge factors (SP only)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
+#pragma unroll
+        for (int yy = 0; yy < C::NYA; ++yy) sgy[yy] = SP ? sponge_gy(prm, y0 - R + re0 + yy) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
         uint32_t smask = 0;                            // sources in this thread's columns/rows of E
         for (int s2 = 0; s2 < prm.nsrc; ++s2)
@@ -175,6 +180,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float *t1 = sP1 + s1 * C::EF;
             const int gz = (int)prm.gz0 + z1;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
+            const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
             const bool store = (z1 >= z0) && (z1 < z1e);
             const bool push1 = PEER && peer_plane(prm.peer1, z1, (int)prm.nz);
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
@@ -211,7 +217,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         for (int m = 1; m <= R; ++m)
                             szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
                         S = inz ? __fadd_rn(S, szz) : S;
-                        f4set(o, e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pm4, e), gz, y, xb + e));
+                        f4set(o, e, time_update<SP>(f4(k4, e), S, pc, f4(pm4, e), sgz, sgy[yy], sgx[e]));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && y < ny;
                     oraw[yy] = o;
@@ -263,6 +269,11 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    float sgx[4], sgy[C::NYB];                         // sponge factors (SP only)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
+#pragma unroll
+    for (int yy = 0; yy < C::NYB; ++yy) sgy[yy] = SP ? sponge_gy(prm, y0 + ri0 + yy) : 1.f;
     uint32_t smask = 0;
     for (int s2 = 0; s2 < prm.nsrc; ++s2)
         if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4 && prm.sy[s2] >= y0 + ri0 && prm.sy[s2] < y0 + ri0 + C::NYB)
@@ -306,6 +317,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         const float *tk = sAux + sab * 2 * C::EF + C::EF;
         const int gz = (int)prm.gz0 + z2;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
+        const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
         float4 out[C::NYB];
         if (act) {
             float4 col[C::NYB + 2 * R];
@@ -336,7 +348,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     for (int m = 1; m <= R; ++m)
                         szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
                     S = inz ? __fadd_rn(S, szz) : S;
-                    f4set(out[yy], e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pk4, e), gz, y, xb + e));
+                    f4set(out[yy], e, time_update<SP>(f4(k4, e), S, pc, f4(pk4, e), sgz, sgy[yy], sgx[e]));
                 }
             }
         }
@@ -475,6 +487,9 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         bool inx[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+        float sgx[4];                                  // sponge factors (SP only)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
         uint32_t smask = 0;
         for (int s2 = 0; s2 < prm.nsrc; ++s2)
@@ -518,7 +533,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         for (int m = 1; m <= R; ++m)
                             szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
                         S = inz ? __fadd_rn(S, szz) : S;
-                        f4set(o, e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pm4, e), gz, 0, xb + e));
+                        f4set(o, e, time_update<SP>(f4(k4, e), S, pc, f4(pm4, e), SP ? sponge_gz(prm, gz) : 1.f,
+                                                    1.f, sgx[e]));
                     }
                     const bool interior = qint && re >= R && re < R + C::TY && z < prm.zhi;
                     oraw[yy] = o;
@@ -558,6 +574,9 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+    float sgx[4];                                      // sponge factors (SP only)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
     uint32_t smask = 0;
     for (int s2 = 0; s2 < prm.nsrc; ++s2)
         if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
@@ -584,6 +603,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4), k4 = lds128(tk + offe);
                 const int gz = (int)prm.gz0 + zt + yy;
                 const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
+                const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const float pc = av[4 + e];
@@ -596,7 +616,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     for (int m = 1; m <= R; ++m)
                         szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
                     S = inz ? __fadd_rn(S, szz) : S;
-                    f4set(out[yy], e, time_update<SP>(prm, f4(k4, e), S, pc, f4(pk4, e), gz, 0, xb + e));
+                    f4set(out[yy], e, time_update<SP>(f4(k4, e), S, pc, f4(pk4, e), sgz, 1.f, sgx[e]));
                 }
             }
         }
