@@ -5,5 +5,5 @@ run() {
   done
 }
 echo "== hint"; run
-FD_NVCC_EXTRA=-DFD_MBAR_SUSPEND_NS=0 python -c "from paper_2311_05038_b200.build import build_lib; build_lib(force=True)"
+FD_NVCC_EXTRA=-DFD_MBAR_SUSPEND_NS=0 python -c "from __graft_entry__ import build_lib; build_lib(force=True)"
 echo "== nohint"; run

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def fd():
-    from paper_2311_05038_b200.build import build_lib
+    from __graft_entry__ import build_lib
     build_lib()
     import paper_2311_05038_b200 as m
     return m

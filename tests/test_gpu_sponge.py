@@ -14,7 +14,7 @@ def fd():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2311_05038_b200.build import build_lib
+    from __graft_entry__ import build_lib
     build_lib()
     import paper_2311_05038_b200 as m
     return m
