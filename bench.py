@@ -290,6 +290,8 @@ def run_ours(args, wl):
     if args.no_graph:
         opts[fd.FD_OPT_GRAPH] = 0
     opts[fd.FD_OPT_TSTEPS] = args.tsteps
+    if args.kplane:
+        opts[fd.FD_OPT_KPLANE] = 1
     sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport,
                     sponge=args.sponge)
     sim.step(args.warmup)
@@ -350,7 +352,8 @@ def run_ours(args, wl):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        s2 = _make_sim(wl, world, vel_pin, gdims, transport=args.transport, sponge=args.sponge)
+        s2 = _make_sim(wl, world, vel_pin, gdims, transport=args.transport, sponge=args.sponge,
+                       options={fd.FD_OPT_KPLANE: 1} if args.kplane else None)
         s2.step(args.steps)
         T2 = s2.traces()
         W2 = s2.wavefield(out=out_pin)
@@ -381,11 +384,13 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     # regions on the comm stream + the interior); their durations are summed
     k_avg_s = kms / max(npass, 1) / 1e3
     # algorithmic bytes per launch: 16 B per point for a one-step launch; a
-    # temporal-blocking launch does two steps for 20 B per point
-    bytes_per_launch = (20.0 if steps_per_launch == 2 else BYTES_PER_POINT) * wl.npts
+    # temporal-blocking launch does two steps for 20 B per point; with K per
+    # plane (--kplane, FD_OPT_KPLANE active) 4 B less (K is not streamed)
+    kz = bool(info.get("kplane"))
+    bytes_per_launch = ((20.0 if steps_per_launch == 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * wl.npts
     achieved = bytes_per_launch / k_avg_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": _ncu_traffic(wl.name, wl.order, ":tb2" if steps_per_launch == 2 else ""),
+            "traffic": _ncu_traffic(wl.name, wl.order, (":tb2" if steps_per_launch == 2 else "") + (":kz" if kz else "")),
             "peak_source": peak_src,
             "algorithmic_bytes_per_point": bytes_per_launch / wl.npts / steps_per_launch,
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
@@ -415,6 +420,8 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
                                    f" halo exchange)") if world > 1 else "1 GPU",
                    **({"shared_gpu": True} if os.environ.get("FD_BENCH_SHARE_GPU") == "1" else {}),
                    **({"sponge_cells": args.sponge} if args.sponge else {}),
+                   **({"k_storage": "per-plane table (FD_OPT_KPLANE; the model is layered)" if kz else
+                       "K field (per-plane table requested, model not plane-constant)"} if args.kplane else {}),
                    "global_grid": [wl.dims[0] * world] + list(wl.dims[1:]),
                    "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -446,6 +453,9 @@ def main(argv=None):
                     help="halo transport at N>1: NCCL send/recv or in-kernel peer stores (CUDA IPC)")
     ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (library default), 1 one step per launch, 2 temporal blocking (10 B/update)")
+    ap.add_argument("--kplane", action="store_true",
+                    help="FD_OPT_KPLANE: K per plane for layered/homogeneous models (12 B per single-step update; "
+                         "not the headline)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     args = ap.parse_args(argv)

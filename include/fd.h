@@ -226,12 +226,22 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *                    boundary-plane launches store their planes into the
  *                    neighbours' halos in the kernel epilogue (virtual slabs: no
  *                    copies; ranks: fd_peer_export / fd_peer_import, flag sync)
+ *   FD_OPT_KPLANE    0 (default) off; 1: when K = (v dt/h)^2/scale is constant on
+ *                    every plane of the slow axis (z in 3D, rows in 2D: layered
+ *                    and homogeneous models), the tiled kernels read K per plane
+ *                    from a table of the same fp32 values instead of streaming
+ *                    the K field (SURVEY 8(f) N4 "reduced-byte K"): 12 B instead
+ *                    of 16 B per single-step update, 16 B instead of 20 B per
+ *                    two-step launch; bitwise the same results.  Checked on the
+ *                    device at the first fd_step (bit equality per plane); if
+ *                    any plane varies the K field is used.  fd_get_info reports
+ *                    which (kplane).  Not with the peer transport across ranks.
  * FD_OPT_ASYNC, FD_OPT_PROFILE and FD_OPT_RESERVE may be set at any time; the others only before
  * the first fd_step.  Errors: FD_ERR_ARG (unknown key / bad value), FD_ERR_STATE. */
 enum { FD_OPT_KERNEL = 1, FD_OPT_TILE = 2, FD_OPT_ZCHUNKS = 3, FD_OPT_ASYNC = 4,
        FD_OPT_GRAPH = 5, FD_OPT_VSLABS = 6, FD_OPT_PROFILE = 7, FD_OPT_TSTEPS = 8,
        FD_OPT_TB2TILE = 9, FD_OPT_RESERVE = 10, FD_OPT_RESIDENT = 11, FD_OPT_CLUSTER = 12,
-       FD_OPT_TRANSPORT = 13 };
+       FD_OPT_TRANSPORT = 13, FD_OPT_KPLANE = 14 };
 fd_status fd_set_option(fd_ctx *ctx, int key, int64_t value);
 
 /* Device time per kernel kind accumulated while FD_OPT_PROFILE = 1 (ms and launch
@@ -258,6 +268,7 @@ typedef struct {
     int steps_per_launch;      /* 2 with temporal blocking (FD_OPT_TSTEPS), 0 when each  */
                                /* fd_step call is one cluster launch (FD_OPT_RESIDENT), else 1 */
     int cluster_ctas;          /* CTAs of the resident cluster (FD_OPT_RESIDENT), else 0 */
+    int kplane;                /* 1 when the kernels read K per plane (FD_OPT_KPLANE)    */
 } fd_info;
 fd_status fd_get_info(fd_ctx *ctx, fd_info *out);
 

@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfd.so"
-SOURCES = [CSRC / "fd_runtime.cu"]
+SOURCES = [CSRC / "fd_runtime.cu"] + sorted(CSRC.glob("fd_tab_*.cu"))
 DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "fd.h"]
 
 NVCC_FLAGS = [
@@ -39,16 +39,34 @@ def needs_build() -> bool:
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> Path:
+    """Compile each translation unit to an object in parallel, then link."""
     if not force and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    from concurrent.futures import ThreadPoolExecutor
+    tag = f"tmp{os.getpid()}"
+    objdir = PKG / "build_obj"
+    objdir.mkdir(exist_ok=True)
     # FD_NVCC_EXTRA: extra nvcc flags for A/B experiments (e.g. -DFD_MBAR_SUSPEND_NS=0)
     extra = os.environ.get("FD_NVCC_EXTRA", "").split()
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES), "-ldl"]
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+        cflags = ["-Xptxas=-v", *cflags]
+    objs = [objdir / f"{src.stem}.{tag}.o" for src in SOURCES]
+
+    def compile_one(i: int) -> None:
+        subprocess.check_call([nvcc(), *cflags, *extra, "-c", "-o", str(objs[i]), str(SOURCES[i])])
+
+    try:
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+            list(ex.map(compile_one, range(len(SOURCES))))
+        tmp = LIB.with_suffix(f".so.{tag}")
+        subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                               "-o", str(tmp), *map(str, objs), "-ldl"])
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if o.exists():
+                o.unlink()
     return LIB
 
 

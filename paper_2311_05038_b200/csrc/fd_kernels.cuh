@@ -35,6 +35,9 @@
 namespace fdk {
 
 constexpr int kMaxSources = 16;
+// FD_OPT_KPLANE tables hold kKzPad zero entries beyond each end of a slab's
+// planes (the 2D row-block kernels evaluate up to one block past zhi)
+constexpr int kKzPad = 512;
 
 // Integer-scaled central second-difference taps (R#2):
 // the exact rationals of order 2r multiplied by scale = 1, 12, 180, 5040.
@@ -102,7 +105,16 @@ struct StepParams {
     int32_t nrec_total;
     PeerPush peer1, peer2;  // in-kernel halo pushes of pnext / pnext2 (boundary launches)
     const float *gsp;       // sponge frame (R#18): g_x[nx], g_y[ny], g_z[nzg] (global z); null = off
+    const float *kz;        // FD_OPT_KPLANE: K of local plane z at kz[z] (z in [-r, nz + r)); the KZ
+                            // kernel variants read it instead of the K field
 };
+
+// Per-plane K (FD_OPT_KPLANE): when K depends on the
+// slow axis only (layered models), the KZ variants take K of plane z from a
+// table of the same fp32 values instead of streaming the K field -- 12 B
+// instead of 16 B per single-step update, bitwise the same result.
+__device__ __forceinline__ float kplane(const StepParams &p, int z) { return __ldg(p.kz + z); }
+__device__ __forceinline__ float4 splat4(float v) { return make_float4(v, v, v, v); }
 
 // Absorbing sponge frame (fd_set_sponge; reading R#18, Cerjan 1985).  The
 // per-axis factors come from the fp32 tables g_x, g_y, g_z (global z); indices
@@ -321,7 +333,7 @@ struct Cfg {
 // grid = ntx * nty * nchunks CTAs; CTA b handles tile (b % ntiles) of z-chunk
 // (b / ntiles) (chunk-major, so co-resident CTAs stream the same z region and
 // share x-y halos in L2).  Warp NWC is the TMA producer; warps 0..NWC-1 compute.
-template <class C, bool SP, bool PEER>
+template <class C, bool SP, bool PEER, bool KZ>
 __global__ void __launch_bounds__(C::NTHREADS)
 fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, BY, 1)
                   const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, TY, 1)
@@ -378,12 +390,13 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                 if (l >= 2 * R) {
                     const int z = j - R, kl = l - 2 * R, ks = kl % C::NSK;
                     mbar_wait(&emptyK[ks], ((kl / C::NSK) & 1) ^ 1);
-                    mbar_expect_tx(&fullK[ks], 2 * C::T_BYTES);
+                    mbar_expect_tx(&fullK[ks], (KZ ? 1 : 2) * C::T_BYTES);
                     float *dst = sK + ks * C::K_FLOATS;
 #pragma unroll
                     for (int pc = 0; pc < C::NTP; ++pc) {
                         tma_load_3d(dst + pc * C::TBW, &map_pp, &fullK[ks], x0 + pc * C::TBW, y0, z + halo_planes(R));
-                        tma_load_3d(dst + C::T_FLOATS + pc * C::TBW, &map_k, &fullK[ks], x0 + pc * C::TBW, y0, z);
+                        if constexpr (!KZ)
+                            tma_load_3d(dst + C::T_FLOATS + pc * C::TBW, &map_k, &fullK[ks], x0 + pc * C::TBW, y0, z);
                     }
                 }
             }
@@ -462,6 +475,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         const int gz = (int)prm.gz0 + z;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
         const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
+        const float kzv = KZ ? kplane(prm, z) : 0.f;
 
         float4 col[C::NY + 2 * C::HY];
         if (C::NDIM == 3) {
@@ -477,7 +491,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w,
                                  R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
-            const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
+            const float4 kk4 = KZ ? splat4(kzv) : lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float pc = a[4 + e];
@@ -596,7 +610,7 @@ struct Cfg2 {
     static_assert(TX % 4 == 0 && TY % NY == 0 && NCONS % 32 == 0, "tile");
 };
 
-template <class C, bool SP, bool PEER>
+template <class C, bool SP, bool PEER, bool KZ>
 __global__ void __launch_bounds__(C::NTHREADS)
 tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box (BX, 1, BZ)
                    const __grid_constant__ CUtensorMap map_pp,   // p_prev buffer, box (TX, 1, TY)
@@ -629,11 +643,11 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
                 const int s = l % C::NS;
                 const int rb = prm.zlo + (b0 + l) * C::TY;          // first local row of the block
                 mbar_wait(&empty[s], ((l / C::NS) & 1) ^ 1);
-                mbar_expect_tx(&full[s], C::STAGE_BYTES);
+                mbar_expect_tx(&full[s], C::STAGE_BYTES - (KZ ? C::T_FLOATS * 4 : 0));
                 float *st = smem + s * C::STAGE;
                 tma_load_3d(st, &map_p, &full[s], x0 - 4, 0, rb - R + halo_planes(R));   // rows rb - r ..
                 tma_load_3d(st + C::P_FLOATS, &map_pp, &full[s], x0, 0, rb + halo_planes(R));
-                tma_load_3d(st + C::P_FLOATS + C::T_FLOATS, &map_k, &full[s], x0, 0, rb);
+                if constexpr (!KZ) tma_load_3d(st + C::P_FLOATS + C::T_FLOATS, &map_k, &full[s], x0, 0, rb);
             }
         }
         return;
@@ -677,7 +691,8 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
             const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
             const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
-            const float4 kk4 = lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
+            const float4 kk4 = KZ ? splat4(kplane(prm, zt + yy))
+                                  : lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
             const int gz = (int)prm.gz0 + zt + yy;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
             const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
@@ -845,7 +860,7 @@ __global__ void gather_receivers_kernel(const StepParams prm) {
 // K = fl32((v dt / h)^2 / scale) in fp64 (R#7), in place over the uploaded
 // velocities of a pitched buffer; explicit _rn intrinsics, so the result is
 // bitwise the host formula ((double)v * dt / h, squared, / scale, rounded once).
-__global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64_t pitch, double dt, double h,
+static __global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64_t pitch, double dt, double h,
                                      double scale) {
     const int64_t total = rows * nx;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -857,18 +872,33 @@ __global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64
 }
 
 // graph bookkeeping: the device step counter
-__global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
+// FD_OPT_KPLANE: table[pl] = K of K-halo-buffer plane pl (pl in [0, planes)),
+// and *bad |= 1 when any in-grid point of a plane differs from its plane's
+// first point (bit comparison; pitch padding excluded).
+static __global__ void kplane_table_kernel(const float *Kh, int64_t planes, int64_t ny, int64_t nx, int64_t pitch,
+                                           float *table, int *bad) {
+    const int64_t n = planes * ny * nx;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pl = i / (ny * nx), rem = i - pl * ny * nx, y = rem / nx, x = rem - y * nx;
+        const float *plane = Kh + pl * ny * pitch;
+        const float ref = plane[0];
+        if (__float_as_uint(plane[y * pitch + x]) != __float_as_uint(ref)) atomicOr(bad, 1);
+        if (rem == 0) table[pl] = ref;
+    }
+}
+
+static __global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
 
 // Peer transport flag sync (fd_runtime.cu peer_signal / peer_wait): the
 // neighbours' flags count completed halo exchanges.  The signal runs after the
 // pushing launches in stream order; the system-scope fence and release store
 // publish their peer stores before the count.
-__global__ void peer_signal_kernel(int64_t *lo, int64_t *hi, int64_t v) {
+static __global__ void peer_signal_kernel(int64_t *lo, int64_t *hi, int64_t v) {
     __threadfence_system();
     if (lo) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(lo), "l"(v) : "memory");
     if (hi) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(hi), "l"(v) : "memory");
 }
-__global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi, int64_t v) {
+static __global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi, int64_t v) {
     for (;;) {
         int64_t a = v, b = v;
         if (need_lo) asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(a) : "l"(flags) : "memory");
@@ -877,7 +907,7 @@ __global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi,
         __nanosleep(200);
     }
 }
-__global__ void advance_step_kernel(int64_t *kdev, int64_t n) { *kdev += n; }
+static __global__ void advance_step_kernel(int64_t *kdev, int64_t n) { *kdev += n; }
 
 // add_source on a field buffer, registration order; records the raw values.
 // field = buffer base; sources with sz outside [0, nz) are skipped (other slab).

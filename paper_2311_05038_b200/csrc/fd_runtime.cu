@@ -19,7 +19,7 @@
 
 #include "../../include/fd.h"
 #include "fd_kernels.cuh"
-#include "fd_tb2.cuh"
+#include "fd_tables.cuh"
 #include "fd_resident.cuh"
 
 using namespace fdk;
@@ -99,128 +99,29 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t nx, int64_t ny, 
     return r == CUDA_SUCCESS;
 }
 
-// ------------------------------------------------------------ kernel table
-typedef void (*launch_fused_t)(dim3, int, cudaStream_t, const CUtensorMap &, const CUtensorMap &,
-                               const CUtensorMap &, const StepParams &);
-
-// Each tiled kernel is compiled in up to four variants v = SP | 2 * PEER:
-// bit 0 the sponge frame (R#18), bit 1 the in-kernel halo pushes of the peer
-// transport.  Tuning-only entries carry variant 0 alone; the configurations
-// the auto policy picks ("full") carry all four.
-struct TileCfg {
-    int ndim, r, tx, ty, ny, dp, dk;
-    int pbw, tbw;        // TMA box widths (halo'd p row piece, p_prev/K row piece)
-    int pbz, tbz;        // TMA box depths in z (2D row blocks; 1 in 3D)
-    int threads, smem;
-    const void *kernel[4];
-    launch_fused_t launch[4];
-    bool full() const { return kernel[3] != nullptr; }
-};
-
-#define FD_LAUNCHER(NAME, KERNEL)                                                                            \
-    template <class C, int V>                                                                                \
-    static void NAME(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,       \
-                     const CUtensorMap &c, const StepParams &p) {                                            \
-        KERNEL<C, (V & 1) != 0, (V & 2) != 0><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);                \
-    }
-FD_LAUNCHER(launch_fused, fused_step_kernel)
-FD_LAUNCHER(launch_tile2d, tile2d_step_kernel)
-FD_LAUNCHER(launch_tb2ws, tb2ws_step_kernel)
-FD_LAUNCHER(launch_tb2d, tb2d_step_kernel)
-
-#define FD_VARIANTS(T, C, FULL, KERNEL, LAUNCH)                                                              \
-    do {                                                                                                     \
-        T.kernel[0] = (const void *)KERNEL<C, false, false>;                                                  \
-        T.launch[0] = LAUNCH<C, 0>;                                                                          \
-        if constexpr (FULL) {                                                                                \
-            T.kernel[1] = (const void *)KERNEL<C, true, false>;                                               \
-            T.kernel[2] = (const void *)KERNEL<C, false, true>;                                               \
-            T.kernel[3] = (const void *)KERNEL<C, true, true>;                                                \
-            T.launch[1] = LAUNCH<C, 1>;                                                                      \
-            T.launch[2] = LAUNCH<C, 2>;                                                                      \
-            T.launch[3] = LAUNCH<C, 3>;                                                                      \
-        }                                                                                                    \
-    } while (0)
-
-template <int R, int NDIM, int TX, int TY, int NY, int DP, int DK, bool FULL = false>
-static TileCfg make_cfg() {
-    using C = Cfg<R, NDIM, TX, TY, NY, DP, DK>;
-    TileCfg t{NDIM, R, TX, TY, NY, DP, DK, C::PBW, C::TBW, 1, 1, C::NTHREADS, C::SMEM_BYTES, {}, {}};
-    FD_VARIANTS(t, C, FULL, fused_step_kernel, launch_fused);
-    return t;
-}
-
-template <int R, int TX, int TY, int NY, int NS, bool FULL = false>
-static TileCfg make_cfg2() {
-    using C = Cfg2<R, TX, TY, NY, NS>;
-    TileCfg t{2, R, TX, TY, NY, NS, 0, C::PBW, C::TBW, C::PBZ, C::TBZ, C::NTHREADS, C::SMEM_BYTES, {}, {}};
-    FD_VARIANTS(t, C, FULL, tile2d_step_kernel, launch_tile2d);
-    return t;
-}
-
-// Compiled tiles (index = position in this table; FD_OPT_TILE selects one).
-// 3D (fused_step_kernel): x-y tiles with rows per thread NY (4 for r <= 2, 2
-// or 1 above, to bound the register queue), p-ring prefetch DP, (p_prev, K)
-// ring prefetch DK.  2D (tile2d_step_kernel): TX columns x TY-row blocks, NS
-// ring slots.  scripts/tune.py sweeps them; choose_tile() encodes the result
-// (the preferred entry per (ndim, r) is the "full" one).
-#define CFG3(R, NY, F1, F2) make_cfg<R, 3, 64, 32, NY, 2, 2>(), make_cfg<R, 3, 128, 32, NY, 2, 2, F2>(), \
-                    make_cfg<R, 3, 64, 16, NY, 2, 2>(), make_cfg<R, 3, 128, 16, NY, 2, 2, F1>(), \
-                    make_cfg<R, 3, 64, 32, NY, 1, 1>(), make_cfg<R, 3, 32, 32, NY, 2, 2>()
-#define CFG3W(R) make_cfg<R, 3, 64, 32, 2, 2, 2>(), make_cfg<R, 3, 32, 32, 2, 2, 2>(), \
-                 make_cfg<R, 3, 64, 16, 2, 2, 2, true>(), make_cfg<R, 3, 128, 16, 2, 2, 2>(), \
-                 make_cfg<R, 3, 64, 16, 1, 2, 2>(), make_cfg<R, 3, 64, 16, 2, 1, 1>()
-#define CFG2(R) make_cfg2<R, 128, 32, 4, 3>(), make_cfg2<R, 128, 16, 4, 4>(), \
-                make_cfg2<R, 64, 32, 4, 4>(), make_cfg2<R, 128, 64, 8, 2>(), \
-                make_cfg2<R, 64, 16, 2, 4>(), make_cfg2<R, 64, 32, 4, 3, true>(), make_cfg2<R, 64, 32, 2, 3>()
+// ------------------------------------------------------------ kernel tables
+// The tiled kernels' compiled configurations live in fd_tab_*.cu (separate
+// translation units, compiled in parallel); fd_tables.cuh declares them.
 static const std::vector<TileCfg> &tile_table() {
-    static const std::vector<TileCfg> t = {CFG3(1, 4, true, false), CFG3(2, 4, false, true), CFG3W(3), CFG3W(4),
-                                           CFG2(1),    CFG2(2),    CFG2(3),    CFG2(4)};
+    static const std::vector<TileCfg> t = [] {
+        std::vector<TileCfg> v;
+        for (auto part : {fdtab::tiles3d_r12, fdtab::tiles3d_r34, fdtab::tiles2d}) {
+            auto p = part();
+            v.insert(v.end(), p.begin(), p.end());
+        }
+        return v;
+    }();
     return t;
 }
-
-// ------------------------------------------------------------------ context
-// Two-steps-per-pass (temporal blocking) tiles, 3D, r <= 2 (fd_tb2.cuh).
-// Presented as TileCfg so the chunking/receiver code is shared: pbw/pbz hold
-// the P^k box (BX0, BY0), tbw/tbz the grown-tile box (BXE, BYE).
-template <int R, int TX, int TY, int NYA, int NYB, int DP, int DA, int D1, int MINB = 1, bool FULL = false>
-static TileCfg make_tb2ws() {
-    using C = CfgWS<R, TX, TY, NYA, NYB, DP, DA, D1, MINB>;
-    TileCfg t{3, R, TX, TY, NYB, DP, DA, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
-    FD_VARIANTS(t, C, FULL, tb2ws_step_kernel, launch_tb2ws);
-    return t;
-}
-template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1, bool FULL = false>
-static TileCfg make_tb2d() {
-    using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB>;
-    TileCfg t{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
-    FD_VARIANTS(t, C, FULL, tb2d_step_kernel, launch_tb2d);
-    return t;
-}
-
 static const std::vector<TileCfg> &tb2_table() {
-    static const std::vector<TileCfg> t = {
-        // 3D r=1, r04 sweep (C3 order 2, scripts/tune.py --tsteps 2): one
-        // 128 x 16 CTA per SM with 6-slot P^k / 5-slot aux rings 581-584 Gpts/s;
-        // the r03 choice (64 x 16, two CTAs per SM, 5/4 slots) 518; 64 x 16 with
-        // 6/5 slots 542; 128 x 16 with 5/4 slots 534; more stage-B warps
-        // (NYB = 2) 481-551
-        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1, true>(), make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1>(),
-        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 3, 1>(), make_tb2ws<1, 64, 16, 2, 4, 3, 3, 1, 2>(),
-        make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
-        // 3D r=2 (order 4 stays on single steps by default: 421 vs <= 320 Gpts/s in r03)
-        make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1, 1, true>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
-        make_tb2ws<2, 64, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<2, 128, 8, 2, 2, 3, 3, 2, 1>(),
-        make_tb2ws<2, 64, 16, 2, 4, 2, 2, 2, 1>(),
-        // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows.  r04 sweep
-        // (C2): order 2 554 Gpts/s (3 stages, two CTAs per SM; 518 with 2) vs
-        // 400 single-step; order 4 486 vs 397; order 6 391 vs 392; order 8 328 vs 385
-        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2, true>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
-        make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
-        make_tb2d<2, 64, 28, 4, 4, 3, 2, 1, true>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
-        make_tb2d<3, 64, 26, 4, 2, 3, 2, 1, true>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
-        make_tb2d<4, 64, 24, 4, 4, 3, 2, 1, true>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
-        make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>()};
+    static const std::vector<TileCfg> t = [] {
+        std::vector<TileCfg> v;
+        for (auto part : {fdtab::tb2ws, fdtab::tb2d}) {
+            auto p = part();
+            v.insert(v.end(), p.begin(), p.end());
+        }
+        return v;
+    }();
     return t;
 }
 
@@ -298,6 +199,7 @@ struct Slab {
     float *K = nullptr;                         // = Kh + r planes (local plane 0)
     float *D[3] = {nullptr, nullptr, nullptr};   // Pxx, Pyy, Pzz (unfused decomposition only)
     float *d_src_raw = nullptr;
+    float *kzt = nullptr;                       // FD_OPT_KPLANE: per-plane K, local plane z at kzt[kKzPad + z]
     CUtensorMap mHalo[4], mTile[4], mK;        // single-step kernel maps per field buffer
     CUtensorMap mP0[4], mPm[4], mKe;           // TB2 maps
     std::vector<Region> regions;                // single-step launches
@@ -354,6 +256,9 @@ struct fd_ctx {
     int32_t *d_res_rec = nullptr;         // receivers sorted by CTA + offsets
     // FD_OPT_TRANSPORT = 1: in-kernel halo pushes (peer stores) instead of copies / NCCL
     int opt_transport = 0;
+    // FD_OPT_KPLANE: K from a per-plane table where it depends on z only
+    int opt_kplane = 0;
+    bool kplane = false;
     struct Peer {
         float *F[4] = {nullptr, nullptr, nullptr, nullptr};   // the neighbour's field buffers (IPC)
         float *Kh = nullptr;
@@ -416,8 +321,8 @@ static fd_status partition(int64_t nz, int nranks, int rank, int64_t *z0, int64_
 static void free_slab(Slab &s) {
     for (auto &d : s.D) { dev_free(d); d = nullptr; }
     for (auto &f : s.F) { dev_free(f); f = nullptr; }
-    dev_free(s.Kh); dev_free(s.d_src_raw);
-    s.Kh = s.K = s.d_src_raw = nullptr;
+    dev_free(s.Kh); dev_free(s.d_src_raw); dev_free(s.kzt);
+    s.Kh = s.K = s.d_src_raw = s.kzt = nullptr;
     for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
     for (auto &r : s.tb2) { dev_free(r.d_rec); r.d_rec = nullptr; }
 }
@@ -596,7 +501,7 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
 // Resident CTAs per SM of a configuration: the minimum over its compiled variants.
 static int occupancy(const TileCfg &t) {
     int best = -1;
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < kVariants; ++v) {
         if (!t.kernel[v]) continue;
         int n = 0;
         cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem);
@@ -659,7 +564,7 @@ static bool preferred(const fd_ctx *c, const TileCfg &t) {
 
 // The sponge frame and the peer transport run the kernel variants compiled
 // for the "full" table entries only.
-static bool needs_full(const fd_ctx *c) { return c->sponge_nb > 0 || c->opt_transport == 1; }
+static bool needs_full(const fd_ctx *c) { return c->sponge_nb > 0 || c->opt_transport == 1 || c->opt_kplane; }
 
 static void choose_tile(fd_ctx *c, int64_t span) {
     (void)span;
@@ -888,6 +793,33 @@ static void split_regions(const fd_ctx *c, const Slab &s, bool overlap, int32_t 
     add(lo_end, hi_beg, false);
 }
 
+// FD_OPT_KPLANE: per slab, the table of K per plane
+// over the K halo buffer's planes (local -r .. nz + r - 1; zero beyond) and
+// a check that every plane is constant.  The tiled kernels' KZ variants run
+// only when all planes of all slabs are; otherwise the K field is used.
+static fd_status build_kplane(fd_ctx *c) {
+    int *d_bad = (int *)dev_alloc(sizeof(int));
+    if (!d_bad) return fail(FD_ERR_NOMEM, "K-plane flag allocation failed");
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    CUDA_TRY(c, cudaMemset(d_bad, 0, sizeof(int)));
+    for (auto &s : c->slabs) {
+        const size_t tb = (size_t)(s.nz + 2 * kKzPad) * 4;
+        s.kzt = (float *)dev_alloc(tb);
+        if (!s.kzt) { dev_free(d_bad); return fail(FD_ERR_NOMEM, "K-plane table allocation failed"); }
+        c->dev_bytes += (double)tb;
+        CUDA_TRY(c, cudaMemset(s.kzt, 0, tb));
+        const int64_t planes = s.nz + 2 * c->R;
+        const int blocks = (int)std::min<int64_t>((planes * c->nyg * c->nxg + 255) / 256, (int64_t)c->nsm * 16);
+        kplane_table_kernel<<<blocks, 256>>>(s.Kh, planes, c->nyg, c->nxg, c->pitch, s.kzt + kKzPad - c->R, d_bad);
+        CUDA_TRY(c, cudaGetLastError());
+    }
+    int bad = 0;
+    CUDA_TRY(c, cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+    dev_free(d_bad);
+    c->kplane = (bad == 0);
+    return FD_OK;
+}
+
 static fd_status prepare(fd_ctx *c) {
     fd_status st = split_virtual(c, c->opt_vslabs);
     if (st) return st;
@@ -940,7 +872,7 @@ static fd_status prepare(fd_ctx *c) {
         choose_tile(c, maxnz);
         if (c->tile < 0) return fail(FD_ERR_CUDA, "no fused kernel configuration fits this device");
         const TileCfg &t = tile_table()[c->tile];
-        for (int v = 0; v < 4; ++v)
+        for (int v = 0; v < kVariants; ++v)
             if (t.kernel[v])
                 CUDA_TRY(c, cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
     }
@@ -1001,7 +933,7 @@ static fd_status prepare(fd_ctx *c) {
         }
         if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
         const TileCfg &t = tb[c->tb2];
-        for (int v = 0; v < 4; ++v)
+        for (int v = 0; v < kVariants; ++v)
             if (t.kernel[v])
                 CUDA_TRY(c, cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem));
         const TileCfg &ts = tile_table()[c->tile];
@@ -1061,6 +993,12 @@ static fd_status prepare(fd_ctx *c) {
         st = exchange(c, {{-1, c->R}}, c->stream);
         if (st) return st;
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    // per-plane K once K and its halos are final (peer-transport ranks receive
+    // K's halos with the first exchange: they keep the K field)
+    if (c->opt_kplane && c->opt_kernel == 0 && !c->resident && !(c->nranks > 1 && c->opt_transport == 1)) {
+        st = build_kplane(c);
+        if (st) return st;
     }
     return FD_OK;
 }
@@ -1128,6 +1066,7 @@ static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepPar
     p.traces = c->d_traces;
     p.nrec_total = (int32_t)c->rec.size();
     p.gsp = c->d_gsp;
+    p.kz = c->kplane ? s.kzt + kKzPad : nullptr;
     // step index: baked (plain launches) or *d_k + offset (graph capture)
     p.k = step_k;
     if (c->capturing) { p.kdev = c->d_k; p.koff = (int32_t)(step_k - c->gk0); }
@@ -1280,7 +1219,7 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     const CUtensorMap &mpp = s.mTile[c->iprev];
     const bool push = c->opt_transport == 1 && g.boundary;
     if (push) set_push(c, s, p, c->iprev, c->opt_tsteps == 2 ? c->H : c->R, -1, 0);
-    const launch_fused_t go = t.launch[(c->d_gsp ? 1 : 0) | (push ? 2 : 0)];
+    const launch_fused_t go = t.launch[(c->d_gsp ? kVarSponge : 0) | (push ? kVarPeer : 0) | (c->kplane ? kVarKPlane : 0)];
     tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
 
@@ -1472,7 +1411,7 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
     const bool push = c->opt_transport == 1 && g.boundary;
     if (push) set_push(c, s, p, f1, c->R, f2, c->H);
-    const launch_fused_t go = t.launch[(c->d_gsp ? 1 : 0) | (push ? 2 : 0)];
+    const launch_fused_t go = t.launch[(c->d_gsp ? kVarSponge : 0) | (push ? kVarPeer : 0) | (c->kplane ? kVarKPlane : 0)];
     tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, m0, mm, s.mKe, p); });
 }
 
@@ -2028,6 +1967,10 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         if (v != 0 && v != 1) return fail(FD_ERR_ARG, "FD_OPT_TRANSPORT must be 0 or 1");
         c->opt_transport = (int)v;
         return FD_OK;
+    case FD_OPT_KPLANE:
+        if (v != 0 && v != 1) return fail(FD_ERR_ARG, "FD_OPT_KPLANE must be 0 or 1");
+        c->opt_kplane = (int)v;
+        return FD_OK;
     case FD_OPT_RESIDENT:
         if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_RESIDENT must be 0, 1 or 2");
         c->opt_resident = (int)v;
@@ -2079,6 +2022,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->order = c->order;
     o->device_bytes = c->dev_bytes;
     o->steps_per_launch = (c->opt_tsteps == 2) ? 2 : 1;
+    o->kplane = c->kplane ? 1 : 0;
     if (c->opt_kernel != 0) { o->kernel = c->opt_kernel; return FD_OK; }
     o->kernel = 2;
     if (c->resident) {

@@ -1,0 +1,28 @@
+// fd_tab_tb2d.cu -- two-steps-per-pass (temporal blocking) tiles, 2D
+// (fd_tb2.cuh; see fd_tables.cuh).
+#define FD_TABLE_TU
+#include "fd_tb2.cuh"
+#include "fd_tables.cuh"
+
+FD_LAUNCHER(launch_tb2d, tb2d_step_kernel)
+
+template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1, bool FULL = false>
+static TileCfg make_tb2d() {
+    using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB>;
+    TileCfg t{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
+    FD_VARIANTS(t, C, FULL, tb2d_step_kernel, launch_tb2d);
+    return t;
+}
+
+std::vector<TileCfg> fdtab::tb2d() {
+    return {
+        // 2D: blocks of 32 - 2r rows, so the grown block is 32 rows.  r04 sweep
+        // (C2): order 2 554 Gpts/s (3 stages, two CTAs per SM; 518 with 2) vs
+        // 400 single-step; order 4 486 vs 397; order 6 391 vs 392; order 8 328 vs 385
+        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2, true>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
+        make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
+        make_tb2d<2, 64, 28, 4, 4, 3, 2, 1, true>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
+        make_tb2d<3, 64, 26, 4, 2, 3, 2, 1, true>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
+        make_tb2d<4, 64, 24, 4, 4, 3, 2, 1, true>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
+        make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>()};
+}

@@ -60,7 +60,7 @@ struct CfgWS {
     static_assert(BX0 <= 256 && BY0 <= 256 && R <= 4, "TMA box");
 };
 
-template <class C, bool SP, bool PEER>
+template <class C, bool SP, bool PEER, bool KZ>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_constant__ CUtensorMap map_pm,
                   const __grid_constant__ CUtensorMap map_k, const StepParams prm) {
@@ -115,10 +115,11 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 if (l >= 2 * R) {
                     const int a = l - 2 * R, z1 = j - R, sa = a % C::NSA;
                     mbar_wait(&emptyA[sa], ((a / C::NSA) & 1) ^ 1);
-                    mbar_expect_tx(&fullA[sa], C::AUX_BYTES);
+                    mbar_expect_tx(&fullA[sa], KZ ? C::AUX_BYTES / 2 : C::AUX_BYTES);
                     float *dst = sAux + sa * 2 * C::EF;
                     tma_load_3d(dst, &map_pm, &fullA[sa], x0 - 4, y0 - R, z1 + halo_planes(R));
-                    tma_load_3d(dst + C::EF, &map_k, &fullA[sa], x0 - 4, y0 - R, z1 + R);   // K halo buffer
+                    if constexpr (!KZ)
+                        tma_load_3d(dst + C::EF, &map_k, &fullA[sa], x0 - 4, y0 - R, z1 + R);   // K halo buffer
                 }
             }
         }
@@ -181,6 +182,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             const int gz = (int)prm.gz0 + z1;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
             const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
+            const float kza = KZ ? kplane(prm, z1) : 0.f;
             const bool store = (z1 >= z0) && (z1 < z1e);
             const bool push1 = PEER && peer_plane(prm.peer1, z1, (int)prm.nz);
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
@@ -197,7 +199,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     const float4 L4 = lds128(row), M4 = qz[R][yy], R4 = lds128(row + 8);
                     const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                     const int offe = re * C::BXE + 4 * q;
-                    const float4 pm4 = lds128(tpm + offe), k4 = lds128(tk + offe);
+                    const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kza) : lds128(tk + offe);
                     const bool iny = (y >= R) && (y < ny - R);
                     float4 o;
 #pragma unroll
@@ -318,6 +320,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         const int gz = (int)prm.gz0 + z2;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
         const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
+        const float kzb = KZ ? kplane(prm, z2) : 0.f;
         float4 out[C::NYB];
         if (act) {
             float4 col[C::NYB + 2 * R];
@@ -329,7 +332,8 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 const int offe = re * C::BXE + 4 * q;
                 const float4 L4 = lds128(t1c + offe - 4), M4 = qz[R][yy], R4 = lds128(t1c + offe + 4);
                 const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
-                const float4 pk4 = lds128(tpk + (re + R) * C::BX0 + 4 * q + 4), k4 = lds128(tk + offe);
+                const float4 pk4 = lds128(tpk + (re + R) * C::BX0 + 4 * q + 4);
+                const float4 k4 = KZ ? splat4(kzb) : lds128(tk + offe);
                 const bool iny = (y >= R) && (y < ny - R);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -428,7 +432,7 @@ struct CfgWS2 {
     static_assert(BX0 <= 256 && BY0 <= 256 && R <= 4, "TMA box");
 };
 
-template <class C, bool SP, bool PEER>
+template <class C, bool SP, bool PEER, bool KZ>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, box (BX0, 1, BY0)
                  const __grid_constant__ CUtensorMap map_pm,   // P^{k-1} buffer, box (BXE, 1, BYE)
@@ -469,11 +473,12 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             for (int l = 0; l < nload; ++l) {
                 const int s = l % C::NS, rb = prm.zlo + (b0 + l) * C::TY;
                 mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
-                mbar_expect_tx(&fullS[s], C::STAGE_BYTES);
+                mbar_expect_tx(&fullS[s], C::STAGE_BYTES - (KZ ? C::BXE * C::BYE * 4 : 0));
                 float *st = sSt + s * C::STAGE;
                 tma_load_3d(st, &map_p0, &fullS[s], x0 - 8, 0, rb - 2 * R + halo_planes(R));        // rows rb-2r.. (+r halo)
                 tma_load_3d(st + C::P0F, &map_pm, &fullS[s], x0 - 4, 0, rb - R + halo_planes(R));   // rows rb-r..
-                tma_load_3d(st + C::P0F + C::EF, &map_k, &fullS[s], x0 - 4, 0, rb);   // K halo buffer: rows rb - r ..
+                if constexpr (!KZ)
+                    tma_load_3d(st + C::P0F + C::EF, &map_k, &fullS[s], x0 - 4, 0, rb);   // K halo buffer: rows rb - r ..
             }
         }
         return;
@@ -517,7 +522,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
                     const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                     const int offe = re * C::BXE + 4 * q;
-                    const float4 pm4 = lds128(tpm + offe), k4 = lds128(tk + offe);
+                    const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kplane(prm, z)) : lds128(tk + offe);
                     const int gz = (int)prm.gz0 + z;
                     const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
                     float4 o;
@@ -600,7 +605,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 const int offe = re * C::BXE + 4 * q;
                 const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
                 const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
-                const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4), k4 = lds128(tk + offe);
+                const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4);
+                const float4 k4 = KZ ? splat4(kplane(prm, zt + yy)) : lds128(tk + offe);
                 const int gz = (int)prm.gz0 + zt + yy;
                 const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
                 const float sgz = SP ? sponge_gz(prm, gz) : 1.f;

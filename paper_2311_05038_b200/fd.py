@@ -23,7 +23,7 @@ FD_FLAG_ALLOW_UNSTABLE = 1
 FD_OPT_KERNEL, FD_OPT_TILE, FD_OPT_ZCHUNKS, FD_OPT_ASYNC, FD_OPT_GRAPH, FD_OPT_VSLABS = 1, 2, 3, 4, 5, 6
 FD_OPT_PROFILE = 7
 FD_OPT_TSTEPS, FD_OPT_TB2TILE, FD_OPT_RESERVE = 8, 9, 10
-FD_OPT_RESIDENT, FD_OPT_CLUSTER, FD_OPT_TRANSPORT = 11, 12, 13
+FD_OPT_RESIDENT, FD_OPT_CLUSTER, FD_OPT_TRANSPORT, FD_OPT_KPLANE = 11, 12, 13, 14
 FD_PEER_BLOB_BYTES = 512
 KERNEL_KINDS = ["fused", "naive", "gather", "inject", "fd_pxx", "fd_pyy", "fd_pzz", "fd_time", "halo",
                 "resident"]
@@ -57,7 +57,7 @@ class FdInfo(ctypes.Structure):
                 ("k_stages", ctypes.c_int), ("ctas", ctypes.c_int), ("threads_per_cta", ctypes.c_int),
                 ("smem_bytes", ctypes.c_int), ("zchunks", ctypes.c_int), ("order", ctypes.c_int),
                 ("device_bytes", ctypes.c_double), ("steps_per_launch", ctypes.c_int),
-                ("cluster_ctas", ctypes.c_int)]
+                ("cluster_ctas", ctypes.c_int), ("kplane", ctypes.c_int)]
 
     def as_dict(self) -> dict:
         d = {}

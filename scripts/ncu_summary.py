@@ -69,10 +69,10 @@ def main(tag):
              "launch of the fused step kernel; launch lists with gpu__time_duration.sum).  Algorithmic bytes",
              "= 16 B x grid points per launch (DESIGN.md section 5.4).", ""]
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
-        m = re.match(rf"prof_{tag}_(C\d)_o(\d)(_tb2)?\.ncu-rep", os.path.basename(rep))
+        m = re.match(rf"prof_{tag}_(C\d)_o(\d)(_tb2)?(_kz)?\.ncu-rep", os.path.basename(rep))
         if not m:
             continue
-        wl, order, tb2 = m.group(1), int(m.group(2)), bool(m.group(3))
+        wl, order, tb2, kz = m.group(1), int(m.group(2)), bool(m.group(3)), bool(m.group(4))
         d = raw(rep)
         kname = d.get("Kernel Name", ("", ""))[0]
         tb2 = tb2 or "tb2" in kname          # the default 3D order-2 path is two steps per launch
@@ -82,11 +82,12 @@ def main(tag):
         dur = float(d["gpu__time_duration.sum"][0].replace(",", ""))
         dunit = d["gpu__time_duration.sum"][1]
         dur_s = dur * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-9)
-        alg = (20.0 if tb2 else 16.0) * npts
-        summ[f"{wl}:o{order}{':tb2' if tb2 else ''}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+        alg = ((20.0 if tb2 else 16.0) - (4.0 if kz else 0.0)) * npts    # K per plane: not streamed
+        summ[f"{wl}:o{order}{':tb2' if tb2 else ''}{':kz' if kz else ''}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                   "algorithmic_bytes": alg, "bytes_per_point": (rd + wr) / npts,
                                   "ncu_duration_s": dur_s, "tag": tag}
-        lines += [f"## {wl}, order {order}{' (temporal blocking, 2 steps per launch)' if tb2 else ''}", "",
+        lines += [f"## {wl}, order {order}{' (temporal blocking, 2 steps per launch)' if tb2 else ''}"
+                  f"{' (K per plane, FD_OPT_KPLANE)' if kz else ''}", "",
                   f"* kernel: `{kname[:120]}`",
                   f"* DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB = {(rd + wr) / npts:.2f} B/pt "
                   f"(algorithmic {alg / npts:.0f} B/pt = {alg / 1e9:.3f} GB)",
