@@ -180,6 +180,17 @@ __device__ __forceinline__ const float *w_next_of(const StepParams &p, int64_t k
     return p.wtab + (k + 1) * p.nsrc;   // w_{k+1}
 }
 
+// Position in an N-slot mbarrier ring: slot and phase parity of a counter
+// advanced by one per plane (instead of a division per use).
+template <int N>
+struct RingPos {
+    int slot = 0;
+    uint32_t par = 0;
+    __device__ __forceinline__ void next() {
+        if (++slot == N) { slot = 0; par ^= 1u; }
+    }
+};
+
 // compile-time loop: f(std::integral_constant<int, B>) ... f(<E-1>)
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F &&f) {
@@ -410,6 +421,13 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     const int yb = y0 + ty * C::NY;               // first of its NY rows
     const int nx = (int)prm.nx, ny = (int)prm.ny;   // 32-bit index math (dims <= 2^30)
     const int cL = C::pcol(4 * tx), cM = C::pcol(4 * tx + 4), cR = C::pcol(4 * tx + 8);
+    const int pitch = (int)prm.pitch;
+    const int64_t pstride = (int64_t)ny * prm.pitch;   // floats per buffer plane
+    const int roff = yb * pitch + xb;             // this thread's first row within a plane
+    uint32_t vmask = 0;                           // rows inside the grid
+#pragma unroll
+    for (int yy = 0; yy < C::NY; ++yy)
+        if (yb + yy < ny) vmask |= 1u << yy;
 
     bool inx[4];
 #pragma unroll
@@ -445,6 +463,9 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 
     constexpr float c0 = tap(R, 0);
     constexpr int Q = 2 * R + 1;
+    RingPos<C::NSP> pl;                 // p load l (full wait)
+    RingPos<C::NSP> pz{C::NSP - R, 0u}; // p load l - r (plane z: x-y taps)
+    RingPos<C::NSK> pk;                 // (p_prev, K) plane kl = l - 2r
 
     // One plane of the stream.  For r <= 2 the register queue rotates instead
     // of shifting: at phase PH (= l mod Q, a compile-time constant) the logical
@@ -453,8 +474,8 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     auto plane = [&](const int l, auto ph) {
         constexpr int PH = decltype(ph)::value;
         const int j = z0 - R + l;
-        const int s = l % C::NSP;
-        mbar_wait(&fullP[s], (l / C::NSP) & 1);
+        const int s = pl.slot;
+        mbar_wait(&fullP[s], pl.par);
         const float *tp = sP + s * C::P_FLOATS;
         // append this thread's column of plane j (logical entry 2r)
 #pragma unroll
@@ -464,13 +485,16 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             __syncwarp();
             if (lane == 0) mbar_arrive(&emptyP[s]);
         }
-        if (l < 2 * R) return;
+        pl.next();
+        if (l < 2 * R) { pz.next(); return; }
 
         const int z = j - R;                       // plane computed now
-        const int sz_ = (l - R) % C::NSP;          // its p tile (x-y taps)
+        const int sz_ = pz.slot;                   // its p tile (x-y taps)
+        pz.next();
         const float *tz = sP + sz_ * C::P_FLOATS;
-        const int kl = l - 2 * R, ks = kl % C::NSK;
-        mbar_wait(&fullK[ks], (kl / C::NSK) & 1);
+        const int ks = pk.slot;
+        mbar_wait(&fullK[ks], pk.par);
+        pk.next();
         const float *tk = sK + ks * C::K_FLOATS;
         const int gz = (int)prm.gz0 + z;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
@@ -551,17 +575,16 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
             }
         }
         // store p_next in place of p_prev (float4; rows outside the grid skipped)
-        if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext + ((int64_t)(z + halo_planes(R)) * ny + yb) * prm.pitch + xb;
+        if (xb < pitch) {
+            float *dst = prm.pnext + (int64_t)(z + halo_planes(R)) * pstride + roff;
 #pragma unroll
             for (int yy = 0; yy < C::NY; ++yy)
-                if (yb + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if ((vmask >> yy) & 1u) *reinterpret_cast<float4 *>(dst + yy * pitch) = out[yy];
             if (PEER && peer_plane(prm.peer1, z, (int)prm.nz)) {
 #pragma unroll
                 for (int yy = 0; yy < C::NY; ++yy)
-                    if (yb + yy < ny)
-                        peer_store4<R>(prm.peer1, z, (int)prm.nz, (int64_t)ny * prm.pitch,
-                                       (int64_t)(yb + yy) * prm.pitch + xb, out[yy]);
+                    if ((vmask >> yy) & 1u)
+                        peer_store4<R>(prm.peer1, z, (int)prm.nz, pstride, (int64_t)(roff + yy * pitch), out[yy]);
             }
         }
     };
@@ -674,11 +697,13 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
     float *const trace_row = trace_row_of(prm, kk);
     const float *const wn = w_next_of(prm, kk);
 
+    RingPos<C::NS> pr;
     for (int l = 0; l < nload; ++l) {
-        const int s = l % C::NS;
+        const int s = pr.slot;
         const int rb = prm.zlo + (b0 + l) * C::TY;
         const int zt = rb + ty * C::NY;                   // first row of this thread
-        mbar_wait(&full[s], (l / C::NS) & 1);
+        mbar_wait(&full[s], pr.par);
+        pr.next();
         const float *tp = smem + s * C::STAGE;
         const float *tk = tp + C::P_FLOATS;
         float4 col[C::NY + 2 * R];

@@ -29,5 +29,9 @@ std::vector<TileCfg> fdtab::tb2ws() {
         // 3D r=2 (order 4 stays on single steps by default: 421 vs <= 320 Gpts/s in r03)
         make_tb2ws<2, 64, 16, 4, 4, 1, 1, 1, 1, true>(), make_tb2ws<2, 64, 16, 2, 4, 1, 1, 1, 2>(),
         make_tb2ws<2, 64, 16, 2, 4, 3, 3, 2, 1>(), make_tb2ws<2, 128, 8, 2, 2, 3, 3, 2, 1>(),
-        make_tb2ws<2, 64, 16, 2, 4, 2, 2, 2, 1>()};
+        make_tb2ws<2, 64, 16, 2, 4, 2, 2, 2, 1>(),
+        // r05 role-balance sweep (3D r=1, 128 x 16): stage-A rows per thread
+        // NYA / stage-B rows NYB -> warps 7+4, 10+8, 7+8, 4+4
+        make_tb2ws<1, 128, 16, 3, 4, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 2, 2, 3, 3, 2, 1>(),
+        make_tb2ws<1, 128, 16, 3, 2, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 6, 4, 3, 3, 2, 1>()};
 }

@@ -24,6 +24,31 @@
 
 namespace fdk {
 
+// Role-barrier arrivals of the A / B warps.  Default: one arrival per warp
+// after __syncwarp (which orders the lanes' shared-memory accesses before lane
+// 0's release-arrive).  FD_TB2_THREAD_ARRIVE=1: every thread arrives (the form
+// compute-sanitizer racecheck can follow).  Per-thread arrivals cost 32x the
+// barrier updates, and each one can wake the warps polling the barrier: ncu
+// r05 counted 12.2 M re-polls (49 M warp instructions, 12 % of the launch) of
+// stage A on empty P1 slots.
+#ifndef FD_TB2_THREAD_ARRIVE
+#define FD_TB2_THREAD_ARRIVE 0
+#endif
+#ifndef FD_TB2_ROTATE
+#define FD_TB2_ROTATE 0
+#endif
+constexpr int kArrivalsPerWarp = FD_TB2_THREAD_ARRIVE ? 32 : 1;
+
+template <class... B>
+__device__ __forceinline__ void role_release(B *...bars) {
+#if FD_TB2_THREAD_ARRIVE
+    (mbar_arrive(bars), ...);
+#else
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) (mbar_arrive(bars), ...);
+#endif
+}
+
 // ------------------------------------------------------------------ warp-specialised variant
 // Same two-step pass, but stage A and stage B run on separate warp groups that
 // overlap (no CTA barrier per plane) and both keep their z taps in a register
@@ -83,11 +108,10 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     const int z0 = prm.zlo + (int)(((int64_t)span * chunk) / prm.nchunks);
     const int z1e = prm.zlo + (int)(((int64_t)span * (chunk + 1)) / prm.nchunks);
     if (tid == 0) {
-        // role barriers count every thread of the arriving warps: each thread
-        // releases its own shared-memory accesses (no reliance on __syncwarp)
-        for (int i = 0; i < C::NSP; ++i) { mbar_init(&fullP[i], 1); mbar_init(&emptyP[i], 32 * (C::NWA + C::NWB)); }
-        for (int i = 0; i < C::NSA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 32 * (C::NWA + C::NWB)); }
-        for (int i = 0; i < C::NS1; ++i) { mbar_init(&full1[i], 32 * C::NWA); mbar_init(&empty1[i], 32 * C::NWB); }
+        // role barriers count the arriving warps (or threads, see role_release)
+        for (int i = 0; i < C::NSP; ++i) { mbar_init(&fullP[i], 1); mbar_init(&emptyP[i], kArrivalsPerWarp * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::NSA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], kArrivalsPerWarp * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::NS1; ++i) { mbar_init(&full1[i], kArrivalsPerWarp * C::NWA); mbar_init(&empty1[i], kArrivalsPerWarp * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -126,6 +150,18 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         return;
     }
 
+    constexpr int Q = 2 * R + 1;
+    const int64_t plane = (int64_t)ny * prm.pitch;   // floats per buffer plane
+    const int pitch = (int)prm.pitch;
+    // The z-tap queues shift by 2r float4 moves per plane (FD_TB2_ROTATE=1
+    // instead unrolls the loops by Q = 2r+1 so that at phase PH = iteration mod
+    // Q the entry of logical position i (plane j - 2r + i) lives in
+    // qz[(PH + i) % Q] -- no moves, but ncu r05: 19 % fewer instructions and
+    // 1.4x the time, instruction-cache misses (no_instruction stalls) and
+    // spills at the 128-register cap).  Ring slots and parities advance
+    // incrementally (RingPos) instead of by divisions, and the per-row
+    // predicates and store offsets are loop invariants.
+
     if (warp < C::NWA) {
         // -------------------------------------------------------------- stage A
         const bool act = tid < C::NTA;
@@ -140,6 +176,16 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
 #pragma unroll
         for (int yy = 0; yy < C::NYA; ++yy) sgy[yy] = SP ? sponge_gy(prm, y0 - R + re0 + yy) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
+        // per row: band rule along y, stored to C (tile interior), offset in a plane
+        uint32_t ymask = 0, stmask = 0;
+        int roff[C::NYA];
+#pragma unroll
+        for (int yy = 0; yy < C::NYA; ++yy) {
+            const int re = re0 + yy, y = y0 - R + re;
+            if (y >= R && y < ny - R) ymask |= 1u << yy;
+            if (act && qint && re >= R && re < R + C::TY && y < ny && xb < pitch) stmask |= 1u << yy;
+            roff[yy] = y * pitch + xb;
+        }
         uint32_t smask = 0;                            // sources in this thread's columns/rows of E
         for (int s2 = 0; s2 < prm.nsrc; ++s2)
             if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4 && prm.sy[s2] >= y0 - R + re0 &&
@@ -147,44 +193,42 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 smask |= 1u << s2;
         float *const trow = trace_row_of(prm, kk);
         const float *const wv = w_next_of(prm, kk);
-        float4 qz[2 * R + 1][C::NYA];
+        float4 qz[Q][C::NYA];
 #pragma unroll
-        for (int i = 0; i < 2 * R + 1; ++i)
+        for (int i = 0; i < Q; ++i)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) qz[i][yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int l = 0; l < nload; ++l) {
-            const int s = l % C::NSP;
-            mbar_wait(&fullP[s], (l / C::NSP) & 1);
-            const float *tp = sP0 + s * C::P0F;
+        RingPos<C::NSP> pl;                            // P^k load l (full wait)
+        RingPos<C::NSP> pz{C::NSP - R, 0u};            // P^k load l - r (plane z1: x-y taps)
+        RingPos<C::NSA> pa;                            // aux plane a
+        RingPos<C::NS1> p1;                            // P1 plane a
+        auto body = [&](const int l, auto ph) {
+            constexpr int PH = decltype(ph)::value;
+            mbar_wait(&fullP[pl.slot], pl.par);
+            const float *tp = sP0 + pl.slot * C::P0F;
 #pragma unroll
-            for (int i = 0; i < 2 * R; ++i)
-#pragma unroll
-                for (int yy = 0; yy < C::NYA; ++yy) qz[i][yy] = qz[i + 1][yy];
-#pragma unroll
-            for (int yy = 0; yy < C::NYA; ++yy) qz[2 * R][yy] = lds128(tp + (re0 + yy + R) * C::BX0 + 4 * q + 4);
+            for (int yy = 0; yy < C::NYA; ++yy)
+                qz[(PH + 2 * R) % Q][yy] = lds128(tp + (re0 + yy + R) * C::BX0 + 4 * q + 4);
             if (l < 2 * R) {
                 // planes below z0 - r are z taps only: A is done with them now;
                 // planes z0 - r .. z0 - 1 still serve A's x-y taps (released there)
-                if (l < R) {
-                    mbar_arrive(&emptyP[s]);
-                }
-                continue;
+                if (l < R) role_release(&emptyP[pl.slot]);
+                pl.next(); pz.next();
+                return;
             }
             const int a = l - 2 * R, z1 = z0 - R + a;
-            const int sz1 = (l - R) % C::NSP;               // P^k plane z1 (x-y taps)
-            const float *tc = sP0 + sz1 * C::P0F;
-            const int sa = a % C::NSA;
-            mbar_wait(&fullA[sa], (a / C::NSA) & 1);
-            const float *tpm = sAux + sa * 2 * C::EF, *tk = tpm + C::EF;
-            const int s1 = a % C::NS1;
-            mbar_wait(&empty1[s1], ((a / C::NS1) & 1) ^ 1);
-            float *t1 = sP1 + s1 * C::EF;
+            const float *tc = sP0 + pz.slot * C::P0F;      // P^k plane z1 (x-y taps)
+            mbar_wait(&fullA[pa.slot], pa.par);
+            const float *tpm = sAux + pa.slot * 2 * C::EF, *tk = tpm + C::EF;
+            mbar_wait(&empty1[p1.slot], p1.par ^ 1u);
+            float *t1 = sP1 + p1.slot * C::EF;
             const int gz = (int)prm.gz0 + z1;
             const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
             const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
             const float kza = KZ ? kplane(prm, z1) : 0.f;
             const bool store = (z1 >= z0) && (z1 < z1e);
             const bool push1 = PEER && peer_plane(prm.peer1, z1, (int)prm.nz);
+            float *const cpl = prm.pnext + (int64_t)(z1 + halo_planes(R)) * plane;
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -194,13 +238,13 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
-                    const int re = re0 + yy, y = y0 - R + re;
+                    const int re = re0 + yy;
                     const float *row = tc + (re + R) * C::BX0 + 4 * q;
-                    const float4 L4 = lds128(row), M4 = qz[R][yy], R4 = lds128(row + 8);
+                    const float4 L4 = lds128(row), M4 = qz[(PH + R) % Q][yy], R4 = lds128(row + 8);
                     const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kza) : lds128(tk + offe);
-                    const bool iny = (y >= R) && (y < ny - R);
+                    const bool iny = (ymask >> yy) & 1u;
                     float4 o;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -217,13 +261,14 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         float szz = __fmul_rn(c0, pc);
 #pragma unroll
                         for (int m = 1; m <= R; ++m)
-                            szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
+                            szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[(PH + R - m) % Q][yy], e),
+                                                                  f4(qz[(PH + R + m) % Q][yy], e)), szz);
                         S = inz ? __fadd_rn(S, szz) : S;
                         f4set(o, e, time_update<SP>(f4(k4, e), S, pc, f4(pm4, e), sgz, sgy[yy], sgx[e]));
                     }
-                    const bool interior = qint && re >= R && re < R + C::TY && y < ny;
                     oraw[yy] = o;
                     if (smask) {                                      // w_{k+1} wherever in E
+                        const int y = y0 - R + re;
                         for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                             if (!((smask >> s2) & 1u) || prm.sz[s2] != z1 || prm.sy[s2] != y) continue;
                             const int dx = prm.sx[s2] - xb;
@@ -231,11 +276,9 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                         }
                     }
                     *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (store && interior && xb < (int)prm.pitch) {
-                        *reinterpret_cast<float4 *>(prm.pnext + ((int64_t)(z1 + halo_planes(R)) * ny + y) * prm.pitch + xb) = o;
-                        if (push1)
-                            peer_store4<R>(prm.peer1, z1, (int)prm.nz, (int64_t)ny * prm.pitch,
-                                           (int64_t)y * prm.pitch + xb, o);
+                    if (store && ((stmask >> yy) & 1u)) {
+                        *reinterpret_cast<float4 *>(cpl + roff[yy]) = o;
+                        if (push1) peer_store4<R>(prm.peer1, z1, (int)prm.nz, plane, (int64_t)roff[yy], o);
                     }
                 }
             }
@@ -252,12 +295,23 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             }
             // P1 plane z1 ready; P^k plane z1 done for A (x-y taps); aux plane z1
             // done for A; planes of P^k below the window are A-done at their read
-            {
-                mbar_arrive(&full1[s1]);
-                mbar_arrive(&emptyP[sz1]);
-                mbar_arrive(&emptyA[sa]);
-            }
+            role_release(&full1[p1.slot], &emptyP[pz.slot], &emptyA[pa.slot]);
+            pl.next(); pz.next(); pa.next(); p1.next();
+        };
+#if FD_TB2_ROTATE
+        for (int l0 = 0; l0 < nload; l0 += Q)
+            static_for<0, Q>([&](auto ph) {
+                if (l0 + decltype(ph)::value < nload) body(l0 + decltype(ph)::value, ph);
+            });
+#else
+        for (int l = 0; l < nload; ++l) {
+#pragma unroll
+            for (int i = 0; i < 2 * R; ++i)
+#pragma unroll
+                for (int yy = 0; yy < C::NYA; ++yy) qz[i][yy] = qz[i + 1][yy];
+            body(l, std::integral_constant<int, 0>{});
         }
+#endif
         // P^k planes z1e + r .. z1e + 2r - 1 (the last r loads) were only z taps: A-done
         // (released when read? they are released by B too); nothing else to release
         return;
@@ -276,47 +330,55 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
 #pragma unroll
     for (int yy = 0; yy < C::NYB; ++yy) sgy[yy] = SP ? sponge_gy(prm, y0 + ri0 + yy) : 1.f;
+    uint32_t ymask = 0, vmask = 0;                     // band rule along y; rows inside the grid
+#pragma unroll
+    for (int yy = 0; yy < C::NYB; ++yy) {
+        const int y = y0 + ri0 + yy;
+        if (y >= R && y < ny - R) ymask |= 1u << yy;
+        if (y < ny) vmask |= 1u << yy;
+    }
+    const int boff = (y0 + ri0) * pitch + xb;          // row ri0 of this thread within a plane
     uint32_t smask = 0;
     for (int s2 = 0; s2 < prm.nsrc; ++s2)
         if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4 && prm.sy[s2] >= y0 + ri0 && prm.sy[s2] < y0 + ri0 + C::NYB)
             smask |= 1u << s2;
     float *const trow = trace_row_of(prm, kk + 1);
     const float *const wv = w_next_of(prm, kk + 1);
-    float4 qz[2 * R + 1][C::NYB];
+    float4 qz[Q][C::NYB];
 #pragma unroll
-    for (int i = 0; i < 2 * R + 1; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
         for (int yy = 0; yy < C::NYB; ++yy) qz[i][yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int a = 0; a < na; ++a) {
-        const int s1 = a % C::NS1;
-        mbar_wait(&full1[s1], (a / C::NS1) & 1);
-        const float *t1n = sP1 + s1 * C::EF;
+    // B's releases run in plane order on every ring: P^k load a, aux plane and
+    // P1 plane 0, 1, ... (warm-up planes as they pass, then plane z2's)
+    RingPos<C::NS1> f1;                                // P1 plane a (full wait)
+    RingPos<C::NSP> rP;                                // P^k load a (= plane z2 for a >= 2r)
+    RingPos<C::NSA> rA;                                // next aux plane to release
+    RingPos<C::NS1> r1;                                // next P1 plane to release
+    auto body = [&](const int a, auto ph) {
+        constexpr int PH = decltype(ph)::value;
+        mbar_wait(&full1[f1.slot], f1.par);
+        const float *t1n = sP1 + f1.slot * C::EF;
 #pragma unroll
-        for (int i = 0; i < 2 * R; ++i)
-#pragma unroll
-            for (int yy = 0; yy < C::NYB; ++yy) qz[i][yy] = qz[i + 1][yy];
-#pragma unroll
-        for (int yy = 0; yy < C::NYB; ++yy) qz[2 * R][yy] = lds128(t1n + (ri0 + yy + R) * C::BXE + 4 * q);
+        for (int yy = 0; yy < C::NYB; ++yy) qz[(PH + 2 * R) % Q][yy] = lds128(t1n + (ri0 + yy + R) * C::BXE + 4 * q);
+        f1.next();
         if (a < 2 * R) {
             // warm-up: B never reads P^k loads 0 .. 2r-1 (it reads P^k at z2 >= z0,
             // load b + r >= 2r) nor aux planes 0 .. r-1; P1 planes 0 .. r-1 are z
             // taps only.  Release them as this iteration passes.
-            {
-                mbar_arrive(&emptyP[a % C::NSP]);
-                if (a < R) {
-                    mbar_arrive(&empty1[s1]);
-                    mbar_arrive(&emptyA[a % C::NSA]);
-                }
+            if (a < R) {
+                role_release(&emptyP[rP.slot], &empty1[r1.slot], &emptyA[rA.slot]);
+                r1.next(); rA.next();
+            } else {
+                role_release(&emptyP[rP.slot]);
             }
-            continue;
+            rP.next();
+            return;
         }
         const int b = a - R, z2 = z0 - R + b;               // plane computed now (>= z0)
-        const int sb1 = b % C::NS1;                         // P1 plane z2 (x-y taps)
-        const float *t1c = sP1 + sb1 * C::EF;
-        const int sp = (b + R) % C::NSP;                    // P^k plane z2 = load b + r
-        const float *tpk = sP0 + sp * C::P0F;
-        const int sab = b % C::NSA;                         // aux plane z2
-        const float *tk = sAux + sab * 2 * C::EF + C::EF;
+        const float *t1c = sP1 + r1.slot * C::EF;           // P1 plane z2 (x-y taps)
+        const float *tpk = sP0 + rP.slot * C::P0F;          // P^k plane z2 = load b + r
+        const float *tk = sAux + rA.slot * 2 * C::EF + C::EF;   // aux plane z2 (K)
         const int gz = (int)prm.gz0 + z2;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
         const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
@@ -328,13 +390,13 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy) {
-                const int re = ri0 + yy + R, y = y0 + ri0 + yy;
+                const int re = ri0 + yy + R;
                 const int offe = re * C::BXE + 4 * q;
-                const float4 L4 = lds128(t1c + offe - 4), M4 = qz[R][yy], R4 = lds128(t1c + offe + 4);
+                const float4 L4 = lds128(t1c + offe - 4), M4 = qz[(PH + R) % Q][yy], R4 = lds128(t1c + offe + 4);
                 const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                 const float4 pk4 = lds128(tpk + (re + R) * C::BX0 + 4 * q + 4);
                 const float4 k4 = KZ ? splat4(kzb) : lds128(tk + offe);
-                const bool iny = (y >= R) && (y < ny - R);
+                const bool iny = (ymask >> yy) & 1u;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const float pc = av[4 + e];
@@ -350,7 +412,8 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     float szz = __fmul_rn(c0, pc);
 #pragma unroll
                     for (int m = 1; m <= R; ++m)
-                        szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[R - m][yy], e), f4(qz[R + m][yy], e)), szz);
+                        szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(qz[(PH + R - m) % Q][yy], e),
+                                                              f4(qz[(PH + R + m) % Q][yy], e)), szz);
                     S = inz ? __fadd_rn(S, szz) : S;
                     f4set(out[yy], e, time_update<SP>(f4(k4, e), S, pc, f4(pk4, e), sgz, sgy[yy], sgx[e]));
                 }
@@ -358,11 +421,8 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         }
         // release: P1 plane z2 (x-y taps done; its column is in the queue), P^k
         // plane z2 (pointwise), aux plane z2 (K)
-        {
-            mbar_arrive(&empty1[sb1]);
-            mbar_arrive(&emptyP[sp]);
-            mbar_arrive(&emptyA[sab]);
-        }
+        role_release(&empty1[r1.slot], &emptyP[rP.slot], &emptyA[rA.slot]);
+        r1.next(); rP.next(); rA.next();
         if (rz == z2) {                                           // owners: B threads
             rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, z2, z2 + 1, trow,
                                      [&](int i, int &ln, int &yy, int &e) {
@@ -374,7 +434,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                                      });
             rz = rp < rend ? prm.rec.z[rp] : INT32_MAX;
         }
-        if (!act) continue;
+        if (!act) return;
         if (smask) {
             for (int s2 = 0; s2 < prm.nsrc; ++s2) {
                 if (!((smask >> s2) & 1u) || prm.sz[s2] != z2) continue;
@@ -388,20 +448,33 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                     }
             }
         }
-        if (xb < (int)prm.pitch) {
-            float *dst = prm.pnext2 + ((int64_t)(z2 + halo_planes(R)) * ny + y0 + ri0) * prm.pitch + xb;
+        if (xb < pitch) {
+            float *dst = prm.pnext2 + (int64_t)(z2 + halo_planes(R)) * plane + boff;
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy)
-                if (y0 + ri0 + yy < ny) *reinterpret_cast<float4 *>(dst + (int64_t)yy * prm.pitch) = out[yy];
+                if ((vmask >> yy) & 1u) *reinterpret_cast<float4 *>(dst + yy * pitch) = out[yy];
             if (PEER && peer_plane(prm.peer2, z2, (int)prm.nz)) {
 #pragma unroll
                 for (int yy = 0; yy < C::NYB; ++yy)
-                    if (y0 + ri0 + yy < ny)
-                        peer_store4<R>(prm.peer2, z2, (int)prm.nz, (int64_t)ny * prm.pitch,
-                                       (int64_t)(y0 + ri0 + yy) * prm.pitch + xb, out[yy]);
+                    if ((vmask >> yy) & 1u)
+                        peer_store4<R>(prm.peer2, z2, (int)prm.nz, plane, (int64_t)(boff + yy * pitch), out[yy]);
             }
         }
+    };
+#if FD_TB2_ROTATE
+    for (int a0 = 0; a0 < na; a0 += Q)
+        static_for<0, Q>([&](auto ph) {
+            if (a0 + decltype(ph)::value < na) body(a0 + decltype(ph)::value, ph);
+        });
+#else
+    for (int a = 0; a < na; ++a) {
+#pragma unroll
+        for (int i = 0; i < 2 * R; ++i)
+#pragma unroll
+            for (int yy = 0; yy < C::NYB; ++yy) qz[i][yy] = qz[i + 1][yy];
+        body(a, std::integral_constant<int, 0>{});
     }
+#endif
 }
 
 
@@ -454,8 +527,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
     const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
     if (tid == 0) {
-        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], 32 * (C::NWA + C::NWB)); }
-        for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], 32 * C::NWA); mbar_init(&empty1[i], 32 * C::NWB); }
+        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], kArrivalsPerWarp * (C::NWA + C::NWB)); }
+        for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], kArrivalsPerWarp * C::NWA); mbar_init(&empty1[i], kArrivalsPerWarp * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -566,7 +639,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                                              ln = t & 31; yy = re % C::NYA; e = dx & 3;
                                              return true;
                                          });
-            { mbar_arrive(&full1[s1]); mbar_arrive(&emptyS[s]); }
+            role_release(&full1[s1], &emptyS[s]);
         }
         return;
     }
@@ -626,7 +699,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 }
             }
         }
-        { mbar_arrive(&empty1[s1]); mbar_arrive(&emptyS[s]); }
+        role_release(&empty1[s1], &emptyS[s]);
         if (rp < rend && prm.rec.z[rp] < rb + C::TY)                  // owners: B threads
             rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
                                      [&](int i, int &ln, int &yy, int &e) {
