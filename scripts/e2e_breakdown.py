@@ -5,7 +5,8 @@
 
 Times fd_create, the first fd_step (setup: buffers, tables, graph capture),
 the remaining steps, fd_get_traces, fd_get_wavefield and fd_destroy with
-pinned host buffers.
+pinned host buffers (FD_TORCH_ALLOC=1: device memory from torch's caching
+allocator, as bench.py).
 """
 import os
 import sys
@@ -22,6 +23,9 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C3"
     order = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1000
+    if os.environ.get("FD_TORCH_ALLOC") == "1":
+        from paper_2311_05038_b200 import fd as fdm
+        fdm.fd_set_allocator_torch()      # as bench.py: torch's caching allocator
     wl = config(name, order=order)
     vel = wl.vel()
     vp = torch.empty(vel.shape, dtype=torch.float32, pin_memory=True).numpy()
