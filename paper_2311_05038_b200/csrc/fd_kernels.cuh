@@ -38,6 +38,12 @@ constexpr int kMaxSources = 16;
 // FD_OPT_KPLANE tables hold kKzPad zero entries beyond each end of a slab's
 // planes (the 2D row-block kernels evaluate up to one block past zhi)
 constexpr int kKzPad = 512;
+// r >= 3 z-tap queues of the single-step 3D kernel shift every kQShift planes
+// (scripts/ab_qshift.sh, C3 order 8: 382 / 390 / 389 / 376 Gpts/s for 1 / 2 / 3 / 4)
+#ifndef FD_QSHIFT
+#define FD_QSHIFT 2
+#endif
+constexpr int kQShift = FD_QSHIFT;
 
 // Integer-scaled central second-difference taps (R#2):
 // the exact rationals of order 2r multiplied by scale = 1, 12, 180, 5040.
@@ -455,14 +461,20 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
     float *const trace_row = trace_row_of(prm, kk);
     const float *const wn = w_next_of(prm, kk);
 
-    float4 q[2 * R + 1][C::NY];
+    // z-tap queue: r <= 2 rotates over Q = 2r+1 entries; r >= 3 keeps
+    // Q + kQShift - 1 entries and shifts by kQShift every kQShift planes
+    constexpr int QU = (2 * R + 1 <= 5) ? 1 : kQShift;
+    constexpr int QN = (QU == 1) ? 2 * R + 1 : 2 * R + QU;
+    float4 q[QN][C::NY];
 #pragma unroll
-    for (int i = 0; i < 2 * R + 1; ++i)
+    for (int i = 0; i < QN; ++i)
 #pragma unroll
         for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     constexpr float c0 = tap(R, 0);
     constexpr int Q = 2 * R + 1;
+    // queue entry of logical position i (plane j - 2r + i) at phase ph
+    auto qslot = [](int ph, int i) constexpr { return QU == 1 ? (ph + i) % Q : ph + i; };
     RingPos<C::NSP> pl;                 // p load l (full wait)
     RingPos<C::NSP> pz{C::NSP - R, 0u}; // p load l - r (plane z: x-y taps)
     RingPos<C::NSK> pk;                 // (p_prev, K) plane kl = l - 2r
@@ -480,7 +492,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         // append this thread's column of plane j (logical entry 2r)
 #pragma unroll
         for (int yy = 0; yy < C::NY; ++yy)
-            q[(PH + 2 * R) % Q][yy] = lds128(tp + (ty * C::NY + yy + C::HY) * C::BX + cM);
+            q[qslot(PH, 2 * R)][yy] = lds128(tp + (ty * C::NY + yy + C::HY) * C::BX + cM);
         if (j < z0 || j >= z1) {               // z-taps only: slot free now
             __syncwarp();
             if (lane == 0) mbar_arrive(&emptyP[s]);
@@ -511,7 +523,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 #pragma unroll
         for (int yy = 0; yy < C::NY; ++yy) {
             const float *row = tz + (ty * C::NY + yy + C::HY) * C::BX;
-            const float4 L4 = lds128(row + cL), M4 = q[(PH + R) % Q][yy], R4 = lds128(row + cR);
+            const float4 L4 = lds128(row + cL), M4 = q[qslot(PH, R)][yy], R4 = lds128(row + cR);
             const float a[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w,
                                  R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
@@ -536,7 +548,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
                     szz = __fmaf_rn(tap(R, m),
-                                    __fadd_rn(f4(q[(PH + R - m) % Q][yy], e), f4(q[(PH + R + m) % Q][yy], e)), szz);
+                                    __fadd_rn(f4(q[qslot(PH, R - m)][yy], e), f4(q[qslot(PH, R + m)][yy], e)), szz);
                 S = inz ? __fadd_rn(S, szz) : S;
                 const float upd = time_update<SP>(f4(kk4, e), S, pc, f4(pp4, e), sgz, sgy[yy], sgx[e]);
                 f4set(out[yy], e, upd);
@@ -595,15 +607,19 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                 if (l0 + decltype(ph)::value < nload) plane(l0 + decltype(ph)::value, ph);
             });
     } else {
-        // r >= 3: the 7-9 body copies cost more in instruction cache than the
-        // 2r moves per point they save (measured: C3 order 8 379 -> 359 Gpts/s);
-        // shift the queue and keep phase 0
-        for (int l = 0; l < nload; ++l) {
+        // r >= 3: full rotation needs 7-9 body copies, which cost more in
+        // instruction cache than the 2r moves per point they save (measured: C3
+        // order 8 379 -> 359 Gpts/s).  Instead kQShift body copies run on a
+        // queue of 2r + kQShift entries (phase PH uses entries PH .. PH + 2r),
+        // then the queue shifts by kQShift: 2r moves per kQShift planes.
+        for (int l0 = 0; l0 < nload; l0 += QU) {
+            static_for<0, QU>([&](auto ph) {
+                if (l0 + decltype(ph)::value < nload) plane(l0 + decltype(ph)::value, ph);
+            });
 #pragma unroll
             for (int i = 0; i < 2 * R; ++i)
 #pragma unroll
-                for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = q[i + 1][yy];
-            plane(l, std::integral_constant<int, 0>{});
+                for (int yy = 0; yy < C::NY; ++yy) q[i][yy] = q[i + QU][yy];
         }
     }
 }
