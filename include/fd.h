@@ -159,8 +159,11 @@ fd_status fd_get_wavefield(fd_ctx *ctx, int which, float *host_out);
 /* Copy the traces recorded so far to host_out as a receiver-major nrec x nsteps matrix
  * (row j = receiver j in registration order).  cap = capacity of host_out in floats;
  * *nsteps_out = steps recorded.  In distributed mode rows of receivers owned by other
- * ranks are exactly 0 (sum across ranks to assemble).
- * Errors: FD_ERR_ARG (null), FD_ERR_STATE (no receivers, or cap < nrec*nsteps), FD_ERR_CUDA. */
+ * ranks are exactly 0 (sum across ranks to assemble).  The transposition from the
+ * device's step-major record runs on the device (a temporary nrec x nsteps buffer);
+ * one copy reaches host_out (pinned host memory makes it a direct DMA).
+ * Errors: FD_ERR_ARG (null), FD_ERR_STATE (no receivers, or cap < nrec*nsteps),
+ * FD_ERR_NOMEM (temporary buffer), FD_ERR_CUDA. */
 fd_status fd_get_traces(fd_ctx *ctx, float *host_out, int64_t cap, int64_t *nsteps_out);
 
 /* Release everything.  NULL -> FD_OK. */

@@ -928,6 +928,27 @@ static __global__ void kplane_table_kernel(const float *Kh, int64_t planes, int6
     }
 }
 
+// fd_get_traces: step-major device traces [k][nrec] -> receiver-major
+// [nrec][k] through 32 x 32 shared-memory tiles (both sides coalesced); rows
+// of receivers this context does not own (own[j] == 0) are written as 0.
+static __global__ void traces_transpose_kernel(const float *in, float *out, int64_t nrec, int64_t k,
+                                               const unsigned char *own) {
+    __shared__ float tile[32][33];
+    const int64_t j0 = (int64_t)blockIdx.x * 32;
+    for (int64_t k0 = (int64_t)blockIdx.y * 32; k0 < k; k0 += (int64_t)gridDim.y * 32) {
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t kk = k0 + r, j = j0 + threadIdx.x;
+            tile[r][threadIdx.x] = (kk < k && j < nrec) ? in[kk * nrec + j] : 0.f;
+        }
+        __syncthreads();
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t j = j0 + r, kk = k0 + threadIdx.x;
+            if (j < nrec && kk < k) out[j * k + kk] = own[j] ? tile[threadIdx.x][r] : 0.f;
+        }
+        __syncthreads();
+    }
+}
+
 static __global__ void set_step_kernel(int64_t *kdev, int64_t k) { *kdev = k; }
 
 // Peer transport flag sync (fd_runtime.cu peer_signal / peer_wait): the

@@ -1750,14 +1750,28 @@ fd_status fd_get_traces(fd_ctx *c, float *host_out, int64_t cap, int64_t *nsteps
         return fail(FD_ERR_STATE, "cap %lld < nrec*nsteps = %lld", (long long)cap, (long long)(nrec * c->k));
     *nsteps_out = c->k;
     if (c->k == 0) return FD_OK;
-    std::vector<float> tmp((size_t)(nrec * c->k));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    CUDA_TRY(c, cudaMemcpy(tmp.data(), c->d_traces, tmp.size() * 4, cudaMemcpyDeviceToHost));
-    // step-major -> receiver-major; rows of receivers owned elsewhere are 0
-    std::vector<char> own((size_t)nrec, 0);
+    // step-major -> receiver-major on the device (rows of receivers owned
+    // elsewhere are 0), then one copy to the host
+    std::vector<unsigned char> own((size_t)nrec, 0);
     for (int64_t j = 0; j < nrec; ++j) own[j] = c->rec[j].g[0] >= c->z0 && c->rec[j].g[0] < c->z1;
-    for (int64_t j = 0; j < nrec; ++j)
-        for (int64_t k = 0; k < c->k; ++k) host_out[j * c->k + k] = own[j] ? tmp[k * nrec + j] : 0.f;
+    const size_t bytes = (size_t)(nrec * c->k) * 4;
+    float *d_out = (float *)dev_alloc(bytes);
+    unsigned char *d_own = (unsigned char *)dev_alloc((size_t)nrec);
+    if (!d_out || !d_own) {
+        dev_free(d_out); dev_free(d_own);
+        return fail(FD_ERR_NOMEM, "trace readback buffer allocation failed");
+    }
+    cudaError_t e = cudaMemcpyAsync(d_own, own.data(), (size_t)nrec, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) {
+        const dim3 grid((unsigned)((nrec + 31) / 32), (unsigned)std::min<int64_t>((c->k + 31) / 32, 65535));
+        traces_transpose_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->d_traces, d_out, nrec, c->k, d_own);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host_out, d_out, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    dev_free(d_out);
+    dev_free(d_own);
+    CUDA_TRY(c, e);
     return FD_OK;
 }
 

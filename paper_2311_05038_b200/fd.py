@@ -212,8 +212,14 @@ def fd_get_wavefield(ctx, which: int, shape, out: np.ndarray | None = None) -> n
     return out
 
 
-def fd_get_traces(ctx, nrec: int, nsteps: int) -> np.ndarray:
-    out = np.empty((nrec, nsteps), dtype=np.float32)
+def fd_get_traces(ctx, nrec: int, nsteps: int, out: np.ndarray | None = None) -> np.ndarray:
+    """Receiver-major traces; ``out``: optional preallocated (e.g. pinned) float32 buffer of >= nrec*nsteps."""
+    if out is None:
+        out = np.empty((nrec, nsteps), dtype=np.float32)
+    else:
+        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < nrec * nsteps:
+            raise ValueError("out must be a C-contiguous float32 array of >= nrec*nsteps elements")
+        out = out.reshape(-1)[: nrec * nsteps].reshape(nrec, nsteps)
     got = ctypes.c_int64()
     _check(lib.fd_get_traces(ctx, out.ctypes.data_as(_f32p), out.size, ctypes.byref(got)), "fd_get_traces")
     return out[:, : got.value] if got.value != nsteps else out
@@ -331,8 +337,9 @@ class Simulation:
     def set_wavefield(self, which: int, field: np.ndarray):
         fd_set_wavefield(self.ctx, which, field)
 
-    def traces(self) -> np.ndarray:
-        return fd_get_traces(self.ctx, self.nrec, self.info()["steps_done"])
+    def traces(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Receiver-major traces (``out``: optional preallocated, e.g. pinned, buffer)."""
+        return fd_get_traces(self.ctx, self.nrec, self.info()["steps_done"], out)
 
     def info(self) -> dict:
         return fd_get_info(self.ctx)

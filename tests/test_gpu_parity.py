@@ -680,3 +680,28 @@ def test_full_size_c3_light_cone(fd, oracle, order, k):
 def test_full_size_c2_light_cone(fd, oracle, order, k):
     from workloads import config
     _cone_case(fd, oracle, config("C2", order=order), k)
+
+
+def test_traces_readback_into_preallocated_buffer(fd):
+    """fd_get_traces transposes on the device; the receiver-major result is the
+    same into a fresh array, a larger preallocated buffer and a pinned one, and
+    each row equals the field sampled at the receiver after every step."""
+    import torch
+    dims = (37, 45)
+    vel = _rand_vel(dims, seed=5)
+    recs = [(int(z), int(x)) for z, x in zip(np.arange(33) % 37, (np.arange(33) * 7) % 45)]   # 33 rows: ragged tile
+    with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_RESIDENT: 1}) as sim:
+        sim.add_source((18, 22), 25.0, 0.02, 1.0)
+        sim.set_receivers(recs)
+        fields = []
+        for _ in range(35):                      # 35 steps: ragged tile in time too
+            sim.step(1)
+            fields.append(sim.wavefield())
+        T = sim.traces()
+        big = np.full(40 * 33, np.nan, np.float32)
+        T2 = sim.traces(out=big)
+        pinned = torch.empty(33 * 35, dtype=torch.float32, pin_memory=True).numpy()
+        T3 = sim.traces(out=pinned)
+    assert T.shape == (33, 35) and np.array_equal(T, T2) and np.array_equal(T, T3)
+    want = np.stack([[f[z, x] for f in fields] for z, x in recs])
+    assert np.array_equal(T, want)
