@@ -454,6 +454,9 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     peak, peak_src = _peaks()
     # dominant kernel: the fused step kernel, one launch per step; its average
     # launch duration from the events around each launch in the timed region
+    # 0: each fd_step(n) call is one cluster launch (FD_OPT_RESIDENT, C1-size
+    # grids): latency-bound, the fraction below is not a roofline statement
+    resident = info.get("steps_per_launch", 1) == 0
     steps_per_launch = int(info.get("steps_per_launch", 1) or 1)
     npass = args.steps // steps_per_launch + args.steps % steps_per_launch
     kms, kn = ktimes.get("fused", (ms_step * args.steps, npass))
@@ -475,13 +478,14 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     kz = bool(info.get("kplane"))
     bytes_per_launch = ((20.0 if steps_per_launch == 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * wl.npts
     achieved = bytes_per_launch / k_avg_s / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+    roof = {"bound": "latency" if resident else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": _ncu_traffic(wl.name, wl.order, (":tb2" if steps_per_launch == 2 else "") + (":kz" if kz else "")),
             "peak_source": peak_src,
             "algorithmic_bytes_per_point": bytes_per_launch / wl.npts / steps_per_launch,
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
             "points_per_launch": wl.npts,
-            "kernel": {(3, 1): "fused_step_kernel", (3, 2): "tb2ws_step_kernel", (2, 1): "tile2d_step_kernel",
+            "kernel": "resident_kernel" if resident else
+                      {(3, 1): "fused_step_kernel", (3, 2): "tb2ws_step_kernel", (2, 1): "tile2d_step_kernel",
                        (2, 2): "tb2d_step_kernel"}[(wl.ndim, steps_per_launch)],
             "kernel_ms_per_launch": k_avg_s * 1e3, "launches_per_pass": kn / max(npass, 1),
             "kernel_ms_per_launch_profile_pass": k_avg_prof_s * 1e3,
