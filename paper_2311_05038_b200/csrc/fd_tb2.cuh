@@ -24,15 +24,15 @@
 
 namespace fdk {
 
-// Role-barrier arrivals of the A / B warps.  Default: one arrival per warp
-// after __syncwarp (which orders the lanes' shared-memory accesses before lane
-// 0's release-arrive).  FD_TB2_THREAD_ARRIVE=1: every thread arrives (the form
-// compute-sanitizer racecheck can follow).  Per-thread arrivals cost 32x the
-// barrier updates, and each one can wake the warps polling the barrier: ncu
-// r05 counted 12.2 M re-polls (49 M warp instructions, 12 % of the launch) of
-// stage A on empty P1 slots.
+// Role-barrier arrivals of the A / B warps.  Default: every thread arrives
+// (each thread releases its own shared-memory accesses -- the form
+// compute-sanitizer racecheck can follow).  FD_TB2_THREAD_ARRIVE=0: one
+// arrival per warp after __syncwarp (which orders the lanes' accesses before
+// lane 0's release-arrive); same speed (r05 A/B: 581.6 vs 581.5 Gpts/s, the
+// same 12.2 M re-polls of stage A on empty P1 slots), but racecheck reports
+// the per-warp form as hazards between A's P1 stores and B's loads.
 #ifndef FD_TB2_THREAD_ARRIVE
-#define FD_TB2_THREAD_ARRIVE 0
+#define FD_TB2_THREAD_ARRIVE 1
 #endif
 #ifndef FD_TB2_ROTATE
 #define FD_TB2_ROTATE 0

@@ -9,7 +9,8 @@
 Covers the fused 3D and 2D kernels (r = 1 and 4, ragged sizes, several
 z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
 naive and unfused reference paths, the two-steps-per-launch kernels
-(3D and 2D, one slab and virtual slabs) and the cluster-resident kernel.
+(3D and 2D, one slab and virtual slabs), the peer-push and sponge variants,
+the per-plane-K (KZ) variants and the cluster-resident kernel.
 """
 import os
 import sys
@@ -29,19 +30,31 @@ def main():
         tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3},
               {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_VSLABS: 3}] \
             if (len(dims) == 2 or order <= 4) else []
+        # per-plane K (KZ variants) needs a layered model: the first half of
+        # the planes at one velocity, the rest at another
+        kz = [{fd.FD_OPT_KPLANE: 1, "layered": True}, {fd.FD_OPT_KPLANE: 1, fd.FD_OPT_TSTEPS: 1, "layered": True},
+              {fd.FD_OPT_KPLANE: 1, fd.FD_OPT_VSLABS: 2, fd.FD_OPT_TRANSPORT: 1, "layered": True}]
         for opts in [{}, {fd.FD_OPT_ZCHUNKS: 3}, {fd.FD_OPT_VSLABS: 2}, {fd.FD_OPT_KERNEL: 1},
-                     {fd.FD_OPT_KERNEL: 3}, {fd.FD_OPT_GRAPH: 0}, {fd.FD_OPT_TSTEPS: 1}] + tb:
+                     {fd.FD_OPT_KERNEL: 3}, {fd.FD_OPT_GRAPH: 0}, {fd.FD_OPT_TSTEPS: 1},
+                     {fd.FD_OPT_VSLABS: 2, fd.FD_OPT_TRANSPORT: 1}, {"sponge": True}] + tb + kz:
             # these small grids would take the cluster-resident path by default:
             # off here, on in its own case below
             opts = {fd.FD_OPT_RESIDENT: 1, **opts}
-            with fd.Simulation(vel, 10.0, 5e-4, order, options=opts) as sim:
+            layered, sponge = opts.pop("layered", False), opts.pop("sponge", False)
+            v = vel
+            if layered:
+                v = np.full(dims, 1800.0, np.float32)
+                v[dims[0] // 2:] = 2300.0
+            with fd.Simulation(v, 10.0, 5e-4, order, options=opts) as sim:
+                if sponge:
+                    sim.set_sponge(4, 0.05)
                 sim.add_source(tuple(d // 2 for d in dims), 25.0, 0.02)
                 sim.set_receivers([tuple(d // 3 for d in dims), tuple(d - 1 for d in dims)])
                 sim.step(20)
                 P = sim.wavefield()
                 T = sim.traces()
                 assert np.all(np.isfinite(P)) and np.all(np.isfinite(T))
-            print("ok", dims, order, opts, flush=True)
+            print("ok", dims, order, opts, "layered" if layered else "", "sponge" if sponge else "", flush=True)
         # whole fd_step calls in one cluster launch (DSMEM halo pushes)
         for ncl in (0, 4):
             with fd.Simulation(vel, 10.0, 5e-4, order,
