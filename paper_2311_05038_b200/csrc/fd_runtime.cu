@@ -436,10 +436,22 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
             th.emplace_back([&, t] {
                 const int64_t a = nloc * t / nt, b = nloc * (t + 1) / nt;
                 float m = 0.f;
-                for (int64_t i = a; i < b; ++i) {
-                    const float v = vloc[i];
-                    if (!(v > 0.f) || !std::isfinite(v)) { bad[t] = i; return; }
-                    m = std::max(m, v);
+                // blocks of 4096 with a branch-free (vectorisable) body; the
+                // first invalid entry is located only in a failing block
+                for (int64_t i0 = a; i0 < b; i0 += 4096) {
+                    const int64_t i1 = std::min<int64_t>(b, i0 + 4096);
+                    int ok = 1;
+                    float bm = 0.f;
+                    for (int64_t i = i0; i < i1; ++i) {
+                        const float v = vloc[i];
+                        ok &= (v > 0.f) & (v <= 3.402823466e38f);     // > 0, not NaN, not +inf
+                        bm = v > bm ? v : bm;
+                    }
+                    if (!ok) {
+                        for (int64_t i = i0; i < i1; ++i)
+                            if (!(vloc[i] > 0.f) || !std::isfinite(vloc[i])) { bad[t] = i; return; }
+                    }
+                    m = std::max(m, bm);
                 }
                 vm[t] = m;
             });
