@@ -231,6 +231,36 @@ def cpu_oracle_sample(wl, budget_s: float = 15.0):
     return wl.npts * steps / el / 1e9, cores, f"{wl.name} full grid {wl.dims}, {steps} steps, {cores} threads"
 
 
+def cpu_oracle_one_thread(wl, budget_s: float = 3.0):
+    """The oracle on ONE host thread (all cores and 1 thread), on a
+    slab of full-width planes sized from a calibration step to ~budget_s."""
+    import oracle
+    from workloads import velocity
+    plane = int(np.prod(wl.dims[1:]))
+    nz_s = max(4 * wl.order + 1, min(wl.dims[0], int(2e6 // plane) + 1))
+    dims_s = (nz_s,) + tuple(wl.dims[1:])
+    vel = velocity(wl.model, dims_s, nz_global=wl.dims[0])
+    src = [((nz_s // 2,) + tuple(s.idx[1:]), s.f, s.t0, s.amp) for s in wl.sources]
+    t0 = time.perf_counter()
+    oracle.run(vel, wl.h, wl.dt, wl.order, 1, src, nthreads=1)
+    t1 = time.perf_counter() - t0
+    steps = int(max(2, min(wl.steps, budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.run(vel, wl.h, wl.dt, wl.order, steps, src, nthreads=1)
+    el = time.perf_counter() - t0
+    return nz_s * plane * steps / el / 1e9, f"{dims_s} slab, {steps} steps, 1 thread"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, wl):
     """The tier's reference arm: the fp64 oracle, as it stands, on the host
     cores.  W warm-up steps, then exactly K timed steps in one oracle call on
@@ -500,7 +530,10 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, desc = cpu_oracle_sample(wl, args.cpu_budget)
-        cpu = {"value": v, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": desc}
+        v1, desc1 = cpu_oracle_one_thread(wl, min(3.0, args.cpu_budget / 5))
+        cpu = {"value": v, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "value_1_thread": v1, "sample_1_thread": desc1, "cpu_model": cpu_model(),
+               "logical_cpus": os.cpu_count()}
     line = {
         "metric": "grid-point updates/s (Gpts/s)", "value": gpts, "unit": "Gpts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
