@@ -44,6 +44,17 @@ constexpr int kKzPad = 512;
 #define FD_QSHIFT 2
 #endif
 constexpr int kQShift = FD_QSHIFT;
+// packed fp32 (FFMA2/FADD2) evaluation of the canonical expression in the
+// single-step 3D kernel's band-rule variants (FD_PACKED=0: scalar).  ncu r05:
+// order 8 242 M -> 199 M warp instructions per launch (it stays on the 16 B/pt
+// memory wall: 389 Gpts/s either way; --kplane 414 -> 423).  The two-step
+// kernel keeps the scalar form: packed, its stage B (one warp per SMSP, the
+// critical chain) lost more to FFMA2 latency and math-pipe throttling than
+// the 9 % fewer instructions gave back (592 vs 601 Gpts/s).
+#ifndef FD_PACKED
+#define FD_PACKED 1
+#endif
+constexpr bool kPackedFp32 = FD_PACKED != 0;
 
 // Integer-scaled central second-difference taps (R#2):
 // the exact rationals of order 2r multiplied by scale = 1, 12, 180, 5040.
@@ -268,6 +279,101 @@ __device__ __forceinline__ float f4(const float4 &v, int e) {
 }
 __device__ __forceinline__ void f4set(float4 &v, int e, float s) {
     if (e == 0) v.x = s; else if (e == 1) v.y = s; else if (e == 2) v.z = s; else v.w = s;
+}
+
+// ------------------------------------------------------------ packed FP32 (sm_100)
+// Blackwell issues two fp32 operations per instruction (FFMA2 / FADD2 /
+// FMUL2, PTX fma/add/mul.rn.f32x2) at the scalar rate in flops
+// (scripts/ffma2_probe.cu: 73.8 vs 72.2 Tflop/s), i.e. half the issue slots.
+// Each lane is the same round-to-nearest operation on the same operands as
+// the scalar instruction, so the packed evaluation is bitwise the canonical
+// per-point expression.  Pairs are (e, e+1) of a thread's 4 x points: the y
+// and z taps and K / p_prev come from float4 registers as aligned pairs;
+// x taps at odd distance straddle two float4s and are summed per lane.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 up2(u64 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// pair (e0, e0+1) of a float4, e0 in {0, 2}
+__device__ __forceinline__ u64 pr2(const float4 &v, int e0) { return e0 == 0 ? pk2(v.x, v.y) : pk2(v.z, v.w); }
+// fma(tap_m, s, acc) per lane; a unit tap is an exact add (as the scalar
+// compiler emits for __fmaf_rn(1, s, acc))
+template <int R, int M>
+__device__ __forceinline__ u64 tapfma2(u64 s, u64 acc) {
+    constexpr float t = tap(R, M);
+    if constexpr (t == 1.0f) return add2(s, acc);
+    else return fma2(pk2(t, t), s, acc);
+}
+
+// One row of a thread: the canonical expression (band rule, no sponge) for
+// its 4 x points, packed.  a = the x row (L4 | M4 | R4, centre M4); yn(o) /
+// zn(o) = the float4 of the y / z neighbour at signed offset o; inx per x
+// point, iny / inz per row / plane; k4, pp4 = K and p_prev.
+template <int R, bool HASY, class YN, class ZN>
+__device__ __forceinline__ float4 stencil_row4(const float (&a)[12], YN yn, ZN zn, const bool (&inx)[4], bool iny,
+                                               bool inz, const float4 &k4, const float4 &pp4) {
+    constexpr float c0 = tap(R, 0);
+    float res[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e0 = 2 * h;
+        const u64 c0pc = mul2(pk2(c0, c0), pk2(a[4 + e0], a[5 + e0]));
+        u64 sx = c0pc;
+        static_for<1, R + 1>([&](auto mm) {
+            constexpr int m = decltype(mm)::value;
+            u64 sum;
+            if constexpr ((m & 1) == 0) sum = add2(pk2(a[4 + e0 - m], a[5 + e0 - m]), pk2(a[4 + e0 + m], a[5 + e0 + m]));
+            else sum = pk2(__fadd_rn(a[4 + e0 - m], a[4 + e0 + m]), __fadd_rn(a[5 + e0 - m], a[5 + e0 + m]));
+            sx = tapfma2<R, m>(sum, sx);
+        });
+        const float2 sxf = up2(sx);
+        u64 S = pk2(inx[e0] ? sxf.x : 0.f, inx[e0 + 1] ? sxf.y : 0.f);
+        if constexpr (HASY) {
+            u64 sy = c0pc;
+            static_for<1, R + 1>([&](auto mm) {
+                constexpr int m = decltype(mm)::value;
+                sy = tapfma2<R, m>(add2(pr2(yn(-m), e0), pr2(yn(m), e0)), sy);
+            });
+            const u64 t = add2(S, sy);
+            S = iny ? t : S;
+        }
+        u64 sz = c0pc;
+        static_for<1, R + 1>([&](auto mm) {
+            constexpr int m = decltype(mm)::value;
+            sz = tapfma2<R, m>(add2(pr2(zn(-m), e0), pr2(zn(m), e0)), sz);
+        });
+        {
+            const u64 t = add2(S, sz);
+            S = inz ? t : S;
+        }
+        const u64 base = pk2(__fmaf_rn(2.f, a[4 + e0], -f4(pp4, e0)), __fmaf_rn(2.f, a[5 + e0], -f4(pp4, e0 + 1)));
+        const float2 o = up2(fma2(pr2(k4, e0), S, base));
+        res[e0] = o.x;
+        res[e0 + 1] = o.y;
+    }
+    return make_float4(res[0], res[1], res[2], res[3]);
 }
 
 
@@ -510,7 +616,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         const float *tk = sK + ks * C::K_FLOATS;
         const int gz = (int)prm.gz0 + z;
         const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
-        const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
+        [[maybe_unused]] const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
         const float kzv = KZ ? kplane(prm, z) : 0.f;
 
         float4 col[C::NY + 2 * C::HY];
@@ -528,6 +634,11 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                                  R4.x, R4.y, R4.z, R4.w};
             const float4 pp4 = lds128(tk + (ty * C::NY + yy) * C::TX + 4 * tx);
             const float4 kk4 = KZ ? splat4(kzv) : lds128(tk + C::T_FLOATS + (ty * C::NY + yy) * C::TX + 4 * tx);
+            if constexpr (!SP && kPackedFp32) {
+                out[yy] = stencil_row4<R, C::NDIM == 3>(
+                    a, [&](int o) { return col[yy + C::HY + o]; }, [&](int o) { return q[qslot(PH, R + o)][yy]; }, inx,
+                    iny[yy], inz, kk4, pp4);
+            } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float pc = a[4 + e];
@@ -552,6 +663,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
                 S = inz ? __fadd_rn(S, szz) : S;
                 const float upd = time_update<SP>(f4(kk4, e), S, pc, f4(pp4, e), sgz, sgy[yy], sgx[e]);
                 f4set(out[yy], e, upd);
+            }
             }
         }
         // release the (p_prev, K) slot and the p slot of plane z (x-y taps done)
