@@ -682,6 +682,15 @@ def test_full_size_c2_light_cone(fd, oracle, order, k):
     _cone_case(fd, oracle, config("C2", order=order), k)
 
 
+@pytest.mark.parametrize("order,k", [(2, 60), (8, 24)])
+def test_full_size_c4_light_cone(fd, oracle, order, k):
+    """C4: 1024^3 HET3D (4.3 GB per field; the strong-scaling base), source 32
+    planes below the top face, so the cone meets the real z boundary."""
+    from workloads import config
+    info = _cone_case(fd, oracle, config("C4", order=order), k)
+    assert info["steps_per_launch"] == (2 if order == 2 else 1)
+
+
 def test_traces_readback_into_preallocated_buffer(fd):
     """fd_get_traces transposes on the device; the receiver-major result is the
     same into a fresh array, a larger preallocated buffer and a pinned one, and
