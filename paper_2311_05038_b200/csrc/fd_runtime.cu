@@ -576,7 +576,10 @@ static bool preferred(const fd_ctx *c, const TileCfg &t) {
 
 // The sponge frame and the peer transport run the kernel variants compiled
 // for the "full" table entries only.
-static bool needs_full(const fd_ctx *c) { return c->sponge_nb > 0 || c->opt_transport == 1 || c->opt_kplane; }
+static bool needs_full(const fd_ctx *c) { return c->sponge_nb > 0 || c->opt_transport == 1; }
+// FD_OPT_KPLANE is optional: a pinned tuning-only tile (no KZ variants) keeps
+// the K field instead of failing
+static bool prefers_full(const fd_ctx *c) { return needs_full(c) || c->opt_kplane; }
 
 static void choose_tile(fd_ctx *c, int64_t span) {
     (void)span;
@@ -588,6 +591,7 @@ static void choose_tile(fd_ctx *c, int64_t span) {
             if (t.ndim != c->ndim || t.r != c->R) continue;
             if (c->opt_tile >= 0 ? i != c->opt_tile : (pass == 0 && !preferred(c, t))) continue;
             if (needs_full(c) && !t.full()) continue;   // sponge / peer variants compiled for full entries
+            if (pass == 0 && c->opt_tile < 0 && prefers_full(c) && !t.full()) continue;
             const int occ = occupancy(t);
             if (occ <= 0) continue;
             bi = i; bocc = occ;
@@ -1008,7 +1012,10 @@ static fd_status prepare(fd_ctx *c) {
     }
     // per-plane K once K and its halos are final (peer-transport ranks receive
     // K's halos with the first exchange: they keep the K field)
-    if (c->opt_kplane && c->opt_kernel == 0 && !c->resident && !(c->nranks > 1 && c->opt_transport == 1)) {
+    const bool kz_compiled = c->tile >= 0 && tile_table()[c->tile].full() &&
+                             (c->opt_tsteps != 2 || (c->tb2 >= 0 && tb2_table()[c->tb2].full()));
+    if (c->opt_kplane && c->opt_kernel == 0 && !c->resident && !(c->nranks > 1 && c->opt_transport == 1) &&
+        kz_compiled) {
         st = build_kplane(c);
         if (st) return st;
     }

@@ -160,3 +160,25 @@ def test_kplane_full_size_bench_config(fd, cfg, order):
     assert a[3]["kplane"] == 0 and b[3]["kplane"] == 1
     _assert_same(a, b, cfg)
     assert np.abs(a[0]).max() > 0
+
+
+def test_kplane_with_pinned_tuning_tile_keeps_the_k_field(fd):
+    """A pinned tuning-only tile (no KZ variants compiled) does not fail: the
+    request is ignored (kplane 0) and the run is bitwise the default one."""
+    from paper_2311_05038_b200 import fd as fdm
+    dims = (40, 36, 70)
+    vel = layered(dims)
+    src, recs = _case(dims)
+    base = {fd.FD_OPT_RESIDENT: 1, fd.FD_OPT_TSTEPS: 1}
+    ref = run(fd, vel, 2, (5, 6), src, recs, options=base)
+    n = 0
+    for tile in range(6):                      # the 3D r=1 entries: one full, five tuning-only
+        try:
+            got = run(fd, vel, 2, (5, 6), src, recs, options={**base, fd.FD_OPT_TILE: tile, fd.FD_OPT_KPLANE: 1})
+        except fdm.FDError as e:
+            assert e.status == fd.FD_ERR_ARG, e   # not an r=1 3D tile
+            continue
+        n += 1
+        _assert_same(got, ref, tile)
+        assert got[3]["kplane"] in (0, 1)
+    assert n >= 2
