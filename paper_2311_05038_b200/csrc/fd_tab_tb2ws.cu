@@ -22,8 +22,9 @@ std::vector<TileCfg> fdtab::tb2ws() {
         // 128 x 16 CTA per SM with 6-slot P^k / 5-slot aux rings 581-584 Gpts/s;
         // the r03 choice (64 x 16, two CTAs per SM, 5/4 slots) 518; 64 x 16 with
         // 6/5 slots 542; 128 x 16 with 5/4 slots 534; more stage-B warps
-        // (NYB = 2) 481-551
-        make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1, true>(), make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1>(),
+        // (NYB = 2) 481-551.  r05 (after the instruction cuts): 7-slot P^k ring
+        // 605 vs 602 (6 slots) -- the default
+        make_tb2ws<1, 128, 16, 2, 4, 4, 3, 2, 1, true>(), make_tb2ws<1, 128, 16, 2, 4, 3, 3, 2, 1>(),
         make_tb2ws<1, 128, 16, 2, 4, 3, 3, 3, 1>(), make_tb2ws<1, 64, 16, 2, 4, 3, 3, 1, 2>(),
         make_tb2ws<1, 64, 16, 2, 4, 2, 2, 2, 2>(), make_tb2ws<1, 128, 8, 2, 2, 2, 2, 2, 2>(),
         // 3D r=2 (order 4 stays on single steps by default: 421 vs <= 320 Gpts/s in r03)
