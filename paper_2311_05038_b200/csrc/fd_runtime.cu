@@ -510,11 +510,18 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
 }
 
 // ------------------------------------------------------------ kernel choice
-// Resident CTAs per SM of a configuration: the minimum over its compiled variants.
-static int occupancy(const TileCfg &t) {
+// Resident CTAs per SM of a configuration: the minimum over the compiled
+// variants this context may launch (band rule or sponge, with or without the
+// peer pushes, with or without per-plane K) -- not over every variant: a
+// heavier unused one must not halve the chunking's slot count.
+static int occupancy(const fd_ctx *c, const TileCfg &t) {
+    const int base = c->sponge_nb > 0 ? kVarSponge : 0;
     int best = -1;
     for (int v = 0; v < kVariants; ++v) {
         if (!t.kernel[v]) continue;
+        if ((v & kVarSponge) != base) continue;
+        if ((v & kVarPeer) && c->opt_transport != 1) continue;
+        if ((v & kVarKPlane) && !c->opt_kplane) continue;
         int n = 0;
         cudaFuncSetAttribute(t.kernel[v], cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, t.kernel[v], t.threads, t.smem) != cudaSuccess) {
@@ -545,7 +552,11 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     // 2D: >= 2 row blocks per chunk
     const int64_t minp = c->ndim == 3 ? std::max(4 * c->R, 8) : 2 * t.ty;
     const int64_t chmax = std::max<int64_t>(1, span / minp);
-    const int64_t waves_target = c->ndim == 3 ? 6 : 3;
+    // 2D two-step launches (tb2d, whose A -> B lag is one row block per chunk)
+    // prefer ~2 full waves of longer chunks (r05 sweep on C2 order 2: 9 chunks
+    // = 1.95 waves 570 Gpts/s vs 13 = 2.8 waves 556)
+    const bool tb2d = c->ndim == 2 && c->tb2 >= 0 && &t == &tb2_table()[c->tb2];
+    const int64_t waves_target = c->ndim == 3 ? 6 : (tb2d ? 2 : 3);
     const int64_t target = std::max<int64_t>(1, (waves_target * slots + ntiles / 2) / ntiles);
     int64_t best = 1;
     double bscore = -1;
@@ -554,7 +565,9 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
         const int64_t units = ntiles * cc, waves = (units + slots - 1) / slots;
         const double fill = (double)units / (double)(waves * slots);
         const double len = (double)span / (double)cc;
-        const double warm = c->ndim == 3 ? c->R : 0.0;        // ~half the 2r warm-up planes' cost
+        // ~half the 2r warm-up planes' cost (3D); the A -> B lag of one row
+        // block per chunk (2D two-step)
+        const double warm = c->ndim == 3 ? c->R : (tb2d ? (double)t.ty : 0.0);
         const double score = fill * len / (len + warm);
         if (score > bscore + 1e-9) { bscore = score; best = cc; }
     }
@@ -592,7 +605,7 @@ static void choose_tile(fd_ctx *c, int64_t span) {
             if (c->opt_tile >= 0 ? i != c->opt_tile : (pass == 0 && !preferred(c, t))) continue;
             if (needs_full(c) && !t.full()) continue;   // sponge / peer variants compiled for full entries
             if (pass == 0 && c->opt_tile < 0 && prefers_full(c) && !t.full()) continue;
-            const int occ = occupancy(t);
+            const int occ = occupancy(c, t);
             if (occ <= 0) continue;
             bi = i; bocc = occ;
             break;
@@ -944,7 +957,7 @@ static fd_status prepare(fd_ctx *c) {
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
             if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
             if (needs_full(c) && !tb[i].full()) continue;
-            const int occ = occupancy(tb[i]);
+            const int occ = occupancy(c, tb[i]);
             if (occ > 0) { c->tb2 = i; c->tb2occ = occ; }
         }
         if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
