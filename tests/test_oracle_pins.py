@@ -556,6 +556,44 @@ def test_green_function_3d():
     assert err0 > 10 * err
 
 
+def test_green_function_2d():
+    """2D counterpart: with the continuum source
+    s(t) = w(t+dt) h^2/dt^2 the trace is
+    T(t) = (h^2 / (dt^2 v^2)) int w(tau + dt) / (2 pi sqrt((t-tau)^2 - R^2/v^2)) dtau
+    over tau < t - R/v.  With t - tau = (R/v) cosh(u) the integrand is smooth:
+    T(t) = (h^2 / (2 pi dt^2 v^2)) int_0^inf w(t + dt - (R/v) cosh u) du.
+    Checked in the window before the boundary reflections return; the
+    no-shift convention (w(tau) instead of w(tau + dt)) is >10x worse."""
+    n, h, v, dt, f, t0, order = 301, 10.0, 2000.0, 0.5e-3, 10.0, 0.15, 8
+    c = n // 2
+    R = 12
+    steps = 640
+    _, _, T = oracle.run(np.full((n, n), v), h, dt, order, steps, [((c, c), f, t0, 1.0)], [(c, c + R)],
+                         nthreads=oracle.max_threads())
+    t = (np.arange(steps) + 1) * dt
+    a = R * h / v
+
+    def w(tt):
+        q = (math.pi * f * (tt - t0)) ** 2
+        return (1 - 2 * q) * np.exp(-q)
+
+    def trace(shift):
+        out = np.empty(steps)
+        for k, tk in enumerate(t):
+            umax = math.acosh(max(1.0, (tk + shift - t0 + 0.5) / a)) + 0.5
+            u = np.linspace(0.0, umax, 20001)
+            g = w(tk + shift - a * np.cosh(u))
+            out[k] = np.sum((g[1:] + g[:-1]) * 0.5) * (u[1] - u[0])
+        return h * h / (2 * math.pi * dt * dt * v * v) * out
+
+    ana, ana0 = trace(dt), trace(0.0)
+    win = t < 0.32                     # the boundary reflection returns after ~1.4 s
+    err = np.linalg.norm(T[0][win] - ana[win]) / np.linalg.norm(ana[win])
+    err0 = np.linalg.norm(T[0][win] - ana0[win]) / np.linalg.norm(ana[win])
+    assert err < 2e-3, err
+    assert err0 > 10 * err, (err0, err)
+
+
 # ---------------------------------------------------------------------------
 # Absorbing sponge frame (SURVEY 8(f) N3, R#18: Cerjan et al. 1985)
 # ---------------------------------------------------------------------------
