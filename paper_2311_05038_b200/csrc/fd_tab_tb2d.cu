@@ -21,7 +21,10 @@ std::vector<TileCfg> fdtab::tb2d() {
         // 400 single-step; order 4 486 vs 397; order 6 391 vs 392; order 8 328 vs 385
         make_tb2d<1, 64, 30, 2, 3, 3, 2, 2, true>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2>(),
         make_tb2d<1, 64, 30, 4, 3, 3, 2>(), make_tb2d<1, 64, 30, 4, 2, 3, 2>(),
-        make_tb2d<2, 64, 28, 4, 4, 3, 2, 1, true>(), make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
+        // order 4 (r05): 40-row blocks, 2 stages, two CTAs per SM 499 vs 490
+        // (28-row blocks, 3 stages: 1.29x vs 1.24x stage-A recomputation)
+        make_tb2d<2, 64, 40, 4, 4, 2, 2, 2, true>(), make_tb2d<2, 64, 28, 4, 4, 3, 2, 1>(),
+        make_tb2d<2, 64, 28, 4, 2, 3, 2>(),
         make_tb2d<3, 64, 26, 4, 2, 3, 2, 1, true>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
         make_tb2d<4, 64, 24, 4, 4, 3, 2, 1, true>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
         make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>()};
