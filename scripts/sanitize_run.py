@@ -24,7 +24,7 @@ sys.path.insert(0, ROOT)
 def main():
     import paper_2311_05038_b200 as fd
     rng = np.random.default_rng(0)
-    cases = [((19, 21, 37), 2), ((23, 18, 41), 8), ((40, 75), 2), ((45, 70), 8)]
+    cases = [((19, 21, 37), 2), ((23, 18, 41), 8), ((40, 75), 2), ((45, 70), 8), ((50, 90), 4)]
     for dims, order in cases:
         vel = rng.uniform(1500, 2500, dims).astype(np.float32)
         tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3},
