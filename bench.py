@@ -251,14 +251,25 @@ def cpu_oracle_one_thread(wl, budget_s: float = 3.0):
     return nz_s * plane * steps / el / 1e9, f"{dims_s} slab, {steps} steps, 1 thread"
 
 
-def cpu_model() -> str:
+def cpu_info() -> dict:
+    """Host CPU as /proc/cpuinfo reports it: model, sockets, physical cores, logical CPUs."""
+    model, sockets, cores = "unknown", set(), set()
     try:
+        phys = None
         for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name":
+                model = v
+            elif k == "physical id":
+                phys = v
+                sockets.add(v)
+            elif k == "core id":
+                cores.add((phys, v))
     except OSError:
         pass
-    return "unknown"
+    return {"cpu_model": model, "sockets": len(sockets) or None, "physical_cores": len(cores) or None,
+            "logical_cpus": os.cpu_count()}
 
 
 def run_reference(args, wl):
@@ -532,8 +543,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
         v, cores, desc = cpu_oracle_sample(wl, args.cpu_budget)
         v1, desc1 = cpu_oracle_one_thread(wl, min(3.0, args.cpu_budget / 5))
         cpu = {"value": v, "unit": "Gpts/s", "cores": cores, "kind": "oracle", "sample": desc,
-               "value_1_thread": v1, "sample_1_thread": desc1, "cpu_model": cpu_model(),
-               "logical_cpus": os.cpu_count()}
+               "value_1_thread": v1, "sample_1_thread": desc1, **cpu_info()}
     line = {
         "metric": "grid-point updates/s (Gpts/s)", "value": gpts, "unit": "Gpts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
