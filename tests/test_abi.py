@@ -109,3 +109,20 @@ def test_unstable_flag_skips_cfl_check(fd):
         fd.fd_destroy(ctx)
     except fd.FDError as e:
         assert e.status == -5   # no CUDA device on a CPU box: not UNSTABLE
+
+
+def test_package_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: importing the binding with libfd.so absent raises
+    ImportError naming the build command (checked in a copy of the package
+    so the real library stays in place)."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = os.path.join(ROOT, "paper_2311_05038_b200")
+    dst = tmp_path / "paper_2311_05038_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "build_obj", "__pycache__"))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "try:\n    import paper_2311_05038_b200\nexcept ImportError as e:\n    print('IMPORTERROR', e)\n"
+            % str(tmp_path))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120).stdout
+    assert "IMPORTERROR" in out and "libfd.so is missing" in out and "no CPU fallback" in out
