@@ -12,6 +12,21 @@ on, W untimed warm-up steps first, max over ranks.  The per-step working set
 (p, p_prev, K: 1.5 GiB for C3) is far larger than the 126 MB L2, so no flush
 is needed between steps (stated in config).
 
+Passes: (1) the value -- K steps replayed from CUDA graphs, CUDA events on
+the library stream, NVML clocks sampled; the roofline's kernel time is this
+region's time / step-kernel launches at N = 1; (2) K more steps with events
+around every launch (per-kernel breakdown; the kernel time at N > 1);
+(3, N = 1, --sustained S) ~S seconds of graph replay after everything else,
+reported as `sustained` with clocks and power (the board's 1 kW cap engages
+after ~0.3 s of full load; not the value).  e2e = three complete public-API
+runs (model upload, K steps, traces and final field to pinned host memory),
+median.  cpu_baseline = the fp64 oracle on a bounded sample, all host cores
+and one.  Device memory comes from torch's caching allocator.
+
+Options: --tsteps 1|2 (steps per launch; 0 auto), --kplane (per-plane K for
+layered/homogeneous models: not the headline), --sponge W (Cerjan frame),
+--transport nccl|peer (N > 1 halo exchange), --no-graph, --no-e2e.
+
 --impl reference times the fp64 CPU oracle (the tier's reference arm) on a
 bounded sample of the same workload on the host cores.
 """
