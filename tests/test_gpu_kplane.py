@@ -146,10 +146,10 @@ def test_kplane_detection(fd, dims):
     assert run(fd, alongx, 2, (3,), src, recs, options=opts)[3]["kplane"] == 0
 
 
-@pytest.mark.parametrize("cfg,order", [("C2", 2), ("C2", 8)])
+@pytest.mark.parametrize("cfg,order", [("C2", 2), ("C2", 8), ("C3", 2), ("C3", 8)])
 def test_kplane_full_size_bench_config(fd, cfg, order):
-    """C2 (4096^2, LAYERED) in the launch configuration bench.py --kplane
-    times: bitwise equal to the K-field run over 40 steps."""
+    """C2 (4096^2, LAYERED) and C3 (512^3, HOMO) in the launch configuration
+    bench.py --kplane times: bitwise equal to the K-field run over 40 steps."""
     from workloads import config
     w = config(cfg, order)
     vel = w.vel()
