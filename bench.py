@@ -25,7 +25,8 @@ and one.  Device memory comes from torch's caching allocator.
 
 Options: --tsteps 1|2 (steps per launch; 0 auto), --kplane (per-plane K for
 layered/homogeneous models: not the headline), --sponge W (Cerjan frame),
---transport nccl|peer (N > 1 halo exchange), --no-graph, --no-e2e.
+--transport nccl|peer (N > 1 halo exchange), --strong (N > 1: split the
+workload's grid instead of stacking N copies), --no-graph, --no-e2e.
 
 --impl reference times the fp64 CPU oracle (the tier's reference arm) on a
 bounded sample of the same workload on the host cores.
@@ -340,16 +341,24 @@ def run_reference(args, wl):
 
 
 # ------------------------------------------------------------------ GPU side
-def _velocity(wl, world):
+def _global_dims(wl, world, strong=False):
+    """The grid all ranks share: the workload's own (N = 1, or --strong: split
+    across the ranks) or N copies stacked along z (weak scaling)."""
+    if world == 1 or strong:
+        return tuple(wl.dims)
+    return (wl.dims[0] * world,) + tuple(wl.dims[1:])
+
+
+def _velocity(wl, world, strong=False):
     """This rank's fp32 velocity planes (the whole grid at N=1)."""
     from workloads import velocity
     if world == 1:
         return wl.vel(), tuple(wl.dims)
     import torch.distributed as dist
     from paper_2311_05038_b200 import dist as fdd
-    gdims = (wl.dims[0] * world,) + tuple(wl.dims[1:])
+    gdims = _global_dims(wl, world, strong)
     z0, z1 = fdd.partition(gdims[0], world, dist.get_rank())
-    return velocity(wl.model, gdims, z0, z1), gdims
+    return velocity(wl.model, gdims, z0, z1, nz_global=gdims[0]), gdims
 
 
 def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl", sponge=0):
@@ -390,7 +399,8 @@ def run_ours(args, wl):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    vel, gdims = _velocity(wl, world)
+    vel, gdims = _velocity(wl, world, args.strong)
+    npts_global = int(np.prod(gdims))
     stream = torch.cuda.Stream(device=dev)
     opts = {fd.FD_OPT_ASYNC: 1}
     if args.no_graph:
@@ -465,7 +475,7 @@ def run_ours(args, wl):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    gpts = wl.npts * args.steps * world / (ms / 1e3) / 1e9
+    gpts = npts_global * args.steps / (ms / 1e3) / 1e9
 
     # e2e through the public API with host buffers (pinned): create (H2D of the
     # model, K computed on the device), K steps, traces + final wavefield read
@@ -499,7 +509,7 @@ def run_ours(args, wl):
     e2e_s = sorted(runs)[1]
     h2d = vel_pin.nbytes + 8 * len(wl.receivers) * wl.ndim
     d2h = T2.nbytes + W2.nbytes
-    e2e = {"value": wl.npts * args.steps * world / e2e_s / 1e9, "unit": "Gpts/s",
+    e2e = {"value": npts_global * args.steps / e2e_s / 1e9, "unit": "Gpts/s",
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": e2e_s, "seconds_runs": runs, "pinned_host_buffers": True,
            "what": "fd_create (model upload) + fd_step(K) + fd_get_traces + fd_get_wavefield",
@@ -542,14 +552,15 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     # temporal-blocking launch does two steps for 20 B per point; with K per
     # plane (--kplane, FD_OPT_KPLANE active) 4 B less (K is not streamed)
     kz = bool(info.get("kplane"))
-    bytes_per_launch = ((20.0 if steps_per_launch == 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * wl.npts
+    npts_local = int(np.prod([d for d in info["local_dims"][:wl.ndim]]))     # this rank's points
+    bytes_per_launch = ((20.0 if steps_per_launch == 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * npts_local
     achieved = bytes_per_launch / k_avg_s / 1e9
     roof = {"bound": "latency" if resident else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": _ncu_traffic(wl.name, wl.order, (":tb2" if steps_per_launch == 2 else "") + (":kz" if kz else "")),
             "peak_source": peak_src,
-            "algorithmic_bytes_per_point": bytes_per_launch / wl.npts / steps_per_launch,
+            "algorithmic_bytes_per_point": bytes_per_launch / npts_local / steps_per_launch,
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
-            "points_per_launch": wl.npts,
+            "points_per_launch": npts_local,
             "kernel": "resident_kernel" if resident else
                       {(3, 1): "fused_step_kernel", (3, 2): "tb2ws_step_kernel", (2, 1): "tile2d_step_kernel",
                        (2, 2): "tb2d_step_kernel"}[(wl.ndim, steps_per_launch)],
@@ -560,7 +571,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
             "kernel_times_ms": {k: v[0] for k, v in ktimes.items()},
             # the Gpts/s ceiling of this kernel's data movement at `peak`, and the
             # value against the one-step-per-launch (16 B/update) ceiling
-            "gpts_ceiling": peak / (bytes_per_launch / wl.npts / steps_per_launch),
+            "gpts_ceiling": peak / (bytes_per_launch / npts_local / steps_per_launch),
             "value_over_single_step_ceiling": gpts * BYTES_PER_POINT / peak / world,
             "kernel_time_source": ksrc}
     cpu = None
@@ -572,7 +583,8 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     line = {
         "metric": "grid-point updates/s (Gpts/s)", "value": gpts, "unit": "Gpts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if (args.strong and world > 1) else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
                    "dt": wl.dt, "h": wl.h, "receivers": len(wl.receivers), "sources": len(wl.sources),
                    "l2": _l2_note(wl),
@@ -582,7 +594,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
                    **({"sponge_cells": args.sponge} if args.sponge else {}),
                    **({"k_storage": "per-plane table (FD_OPT_KPLANE; the model is layered)" if kz else
                        "K field (per-plane table requested, model not plane-constant)"} if args.kplane else {}),
-                   "global_grid": [wl.dims[0] * world] + list(wl.dims[1:]),
+                   "global_grid": list(_global_dims(wl, world, args.strong)),
                    "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "traces_finite": finite,
@@ -616,6 +628,9 @@ def main(argv=None):
                     help="0 auto (library default), 1 one step per launch, 2 temporal blocking (10 B/update)")
     ap.add_argument("--sustained", type=float, default=2.0,
                     help="seconds of an extra graph-replay pass reported as 'sustained' (power-capped state); 0 = off")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: split the workload's grid across the ranks (strong scaling, BASELINE configs[3]) "
+                         "instead of stacking N copies along z (weak scaling, the default)")
     ap.add_argument("--kplane", action="store_true",
                     help="FD_OPT_KPLANE: K per plane for layered/homogeneous models (12 B per single-step update; "
                          "not the headline)")

@@ -97,15 +97,18 @@ def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
         assert np.array_equal(got[f"T{ci}"], ref[2]), ci
 
 
-def test_bench_two_ranks_peer_transport_shared_gpu(fd):
+@pytest.mark.parametrize("strong", [False, True])
+def test_bench_two_ranks_peer_transport_shared_gpu(fd, strong):
     """bench.py's N>1 path end to end (torchrun, barriers, max over ranks, e2e,
     one JSON line from rank 0) with the peer transport, both ranks on the one
-    GPU of this run (FD_BENCH_SHARE_GPU test hook; not a scaling number)."""
+    GPU of this run (FD_BENCH_SHARE_GPU test hook; not a scaling number):
+    weak (N stacked copies) and --strong (the grid split across the ranks)."""
     import json
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
-           "127.0.0.1", "--master-port", str(29800 + os.getpid() % 100), os.path.join(ROOT, "bench.py"),
+           "127.0.0.1", "--master-port", str(29800 + os.getpid() % 100 + (1 if strong else 0)),
+           os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "20", "--warmup", "3", "--config", "C1", "--transport", "peer",
-           "--no-cpu-baseline"]
+           "--no-cpu-baseline"] + (["--strong"] if strong else [])
     env = {**os.environ, "FD_BENCH_SHARE_GPU": "1", "PYTHONPATH": ROOT}
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
@@ -113,5 +116,7 @@ def test_bench_two_ranks_peer_transport_shared_gpu(fd):
     assert len(lines) == 1, res.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["traces_finite"]
-    assert d["config"]["global_grid"][0] == 2 * d["config"]["grid"][0]
+    assert d["config"]["global_grid"][0] == (1 if strong else 2) * d["config"]["grid"][0]
+    assert d["scaling"] == ("strong" if strong else "weak")
+    assert d["roofline"]["points_per_launch"] == (d["config"]["grid"][0] // (2 if strong else 1)) * d["config"]["grid"][1]
     assert "peer" in d["config"]["parallelism"] and d["config"]["shared_gpu"]
