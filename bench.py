@@ -372,8 +372,8 @@ def _make_sim(wl, world, vel, gdims, stream=None, options=None, transport="nccl"
     else:
         from paper_2311_05038_b200 import dist as fdd
         sim = fdd.create(vel, gdims, wl.h, wl.dt, wl.order, device=dist_env()[2], stream=stream,
-                         options=options, transport=transport)
-    if sponge:
+                         options=options, transport=transport, sponge=(sponge, 0.015) if sponge else None)
+    if sponge and world == 1:
         sim.set_sponge(sponge, 0.015)        # Cerjan frame (R#18), classic alpha
     for s in wl.sources:
         sim.add_source(s.idx, s.f, s.t0, s.amp)

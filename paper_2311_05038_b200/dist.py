@@ -33,8 +33,13 @@ def bootstrap_nccl_id(make_id=None) -> bytes:
 
 def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *, device: int = -1,
            nccl_id: bytes | None = None, flags: int = 0, options: dict | None = None,
-           stream: int | None = None, transport: str = "nccl") -> "_fd.Simulation":
+           stream: int | None = None, transport: str = "nccl",
+           sponge: tuple | None = None) -> "_fd.Simulation":
     """Create this rank's slab context; ``vel_slab`` holds only the owned planes.
+
+    ``sponge``: (width, alpha) of the absorbing frame (fd_set_sponge), applied
+    here because the peer transport fixes the context's configuration when
+    it exchanges the IPC blobs below.
 
     ``transport``: "nccl" (halo send/recv on the library's comm stream) or
     "peer" (FD_OPT_TRANSPORT=1: the boundary launches store their planes into
@@ -55,6 +60,8 @@ def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *
                              dist={"global_dims": tuple(global_dims), "rank": rank, "nranks": world,
                                    "device": device, "nccl_id": nccl_id, "vel_is_slab": True},
                              options=options, stream=stream)
+        if sponge:
+            sim.set_sponge(*sponge)
     except _fd.FDError as e:
         err = e
     # every rank must have a context before anyone steps (NCCL is initialised

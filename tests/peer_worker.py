@@ -13,10 +13,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CASES = [  # dims, order, fd_step call lengths
-    ((40, 30, 70), 2, (1, 2, 17, 6)),      # two steps per launch (2r-plane boundary regions)
-    ((37, 26, 45), 8, (3, 12)),            # single steps, r = 4
-    ((90, 140), 4, (5, 20)),               # 2D two-step
+CASES = [  # dims, order, fd_step call lengths, sponge frame (width, alpha) or None
+    ((40, 30, 70), 2, (1, 2, 17, 6), None),        # two steps per launch (2r-plane boundary regions)
+    ((37, 26, 45), 8, (3, 12), None),              # single steps, r = 4
+    ((90, 140), 4, (5, 20), None),                 # 2D two-step
+    ((42, 30, 60), 2, (3, 30), (6, 0.07)),         # sponge frame (global-z factors on every rank)
 ]
 
 
@@ -27,7 +28,7 @@ def main():
     from paper_2311_05038_b200 import dist as fdd
     rank, world = dist.get_rank(), dist.get_world_size()
     out = {}
-    for ci, (dims, order, seq) in enumerate(CASES):
+    for ci, (dims, order, seq, sponge) in enumerate(CASES):
         vel = np.random.default_rng(ci).uniform(1500, 2500, dims).astype(np.float32)
         z0, z1 = fdd.partition(dims[0], world, rank)
         rest = tuple(d // 2 for d in dims[1:])
@@ -35,7 +36,7 @@ def main():
         src = [((f1,) + rest, 25.0, 0.02, 1.0), ((f1 - 1,) + rest, 15.0, 0.03, -0.5)]
         recs = [(f1 - 1,) + rest, (f1,) + rest, (dims[0] - 3,) + rest]
         sim = fdd.create(vel[z0:z1], dims, 10.0, 5e-4, order, device=0, transport="peer",
-                         options={fd.FD_OPT_RESIDENT: 1})
+                         options={fd.FD_OPT_RESIDENT: 1}, sponge=sponge)
         for s in src:
             sim.add_source(*s)
         sim.set_receivers(recs)

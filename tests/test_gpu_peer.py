@@ -78,7 +78,7 @@ def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     got = np.load(out)
-    for ci, (dims, order, seq) in enumerate(worker.CASES):
+    for ci, (dims, order, seq, sponge) in enumerate(worker.CASES):
         vel = np.random.default_rng(ci).uniform(1500, 2500, dims).astype(np.float32)
         rest = tuple(d // 2 for d in dims[1:])
         from paper_2311_05038_b200.dist import partition
@@ -86,6 +86,8 @@ def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
         src = [((f1,) + rest, 25.0, 0.02, 1.0), ((f1 - 1,) + rest, 15.0, 0.03, -0.5)]
         recs = [(f1 - 1,) + rest, (f1,) + rest, (dims[0] - 3,) + rest]
         with fd.Simulation(vel, 10.0, 5e-4, order, options={fd.FD_OPT_RESIDENT: 1, fd.FD_OPT_TSTEPS: 1}) as sim:
+            if sponge:
+                sim.set_sponge(*sponge)
             for s in src:
                 sim.add_source(*s)
             sim.set_receivers(recs)
@@ -102,13 +104,14 @@ def test_bench_two_ranks_peer_transport_shared_gpu(fd, strong):
     """bench.py's N>1 path end to end (torchrun, barriers, max over ranks, e2e,
     one JSON line from rank 0) with the peer transport, both ranks on the one
     GPU of this run (FD_BENCH_SHARE_GPU test hook; not a scaling number):
-    weak (N stacked copies) and --strong (the grid split across the ranks)."""
+    weak (N stacked copies) and --strong (the grid split across the ranks,
+    with the sponge frame, which the peer transport needs at creation)."""
     import json
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
            "127.0.0.1", "--master-port", str(29800 + os.getpid() % 100 + (1 if strong else 0)),
            os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "20", "--warmup", "3", "--config", "C1", "--transport", "peer",
-           "--no-cpu-baseline"] + (["--strong"] if strong else [])
+           "--no-cpu-baseline"] + (["--strong", "--sponge", "8"] if strong else [])
     env = {**os.environ, "FD_BENCH_SHARE_GPU": "1", "PYTHONPATH": ROOT}
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
