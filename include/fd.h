@@ -114,6 +114,15 @@ fd_status fd_nccl_get_unique_id(void *out128);
 enum { FD_PEER_BLOB_BYTES = 512 };
 fd_status fd_peer_export(fd_ctx *ctx, void *blob, size_t cap, size_t *len);
 fd_status fd_peer_import(fd_ctx *ctx, const void *lo_blob, const void *hi_blob);
+/* Teardown of the peer transport (collective order): every rank
+ * calls fd_peer_detach -- it synchronises the context's streams (its last
+ * pushes and signals into the neighbours' memory are done) and closes the IPC
+ * mappings -- then a barrier, then fd_destroy (which frees the exported
+ * buffers).  No fd_step afterwards (FD_ERR_STATE).  A no-op on other contexts.
+ * A neighbour that stops signalling (failed or exited rank) is detected by a
+ * bounded wait (FD_PEER_TIMEOUT_S seconds, default 60): the next fd_step returns
+ * FD_ERR_STATE and the context is poisoned.  Errors: FD_ERR_ARG, FD_ERR_CUDA. */
+fd_status fd_peer_detach(fd_ctx *ctx);
 
 /* Absorbing sponge frame (reading R#18 -- the paper is silent on
  * boundaries, the band rule R#3 stays on the derivatives).  Cerjan et al. (1985):

@@ -1072,12 +1072,27 @@ static __global__ void peer_signal_kernel(int64_t *lo, int64_t *hi, int64_t v) {
     if (lo) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(lo), "l"(v) : "memory");
     if (hi) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(hi), "l"(v) : "memory");
 }
-static __global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi, int64_t v) {
+// Spins until both neighbours have signalled exchange v.  Bounded: after
+// timeout_ns (%globaltimer) it raises *err (mapped host memory; fd_step polls it
+// and poisons the context) and returns, so a neighbour that died does not hang
+// the stream forever; once *err is set every later wait returns at once.
+static __global__ void peer_wait_kernel(const int64_t *flags, int need_lo, int need_hi, int64_t v,
+                                        volatile int *err, uint64_t timeout_ns) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         int64_t a = v, b = v;
         if (need_lo) asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(a) : "l"(flags) : "memory");
         if (need_hi) asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(b) : "l"(flags + 1) : "memory");
         if (a >= v && b >= v) break;
+        if (*err) return;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+            *err = 1;
+            __threadfence_system();
+            return;
+        }
         __nanosleep(200);
     }
 }

@@ -269,6 +269,8 @@ struct fd_ctx {
     bool peer_imported = false;
     bool frozen = false;                  // fd_peer_export done: options fixed
     int64_t *d_flags = nullptr;           // [0]: written by rank - 1, [1]: by rank + 1 (exchange counts)
+    int *h_perr = nullptr, *d_perr = nullptr;   // peer_wait timeout flag (mapped pinned host int)
+    bool peer_detached = false;           // fd_peer_detach done: no more steps
     int64_t xcount = 0;                   // exchanges this rank has signalled
     // absorbing sponge frame (fd_set_sponge, R#18)
     int sponge_nb = 0;
@@ -347,6 +349,8 @@ static void destroy_all(fd_ctx *c) {
     c->plo.opened.clear(); c->phi.opened.clear();
     if (c->d_flags) cudaFree(c->d_flags);
     c->d_flags = nullptr;
+    if (c->h_perr) cudaFreeHost(c->h_perr);
+    c->h_perr = c->d_perr = nullptr;
     c->d_traces = nullptr; c->d_wtab = nullptr; c->d_k = nullptr; c->d_res_rec = nullptr;
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     c->own_stream = nullptr;
@@ -412,6 +416,11 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     int64_t nzg = dims[0], nyg = ndim == 3 ? dims[1] : 1, nxg = dims[ndim - 1];
     if (nxg > (int64_t)1 << 30 || nyg > (int64_t)1 << 30 || nzg > (int64_t)1 << 30)
         return fail(FD_ERR_ARG, "dims too large");
+    // the step kernels keep in-plane offsets (y * pitch + x, pitch = nx rounded
+    // up to 32 floats) in 32 bits; one 64-bit base per plane
+    if (ndim == 3 && (nyg + 4 * R) * ((nxg + 31) / 32 * 32 + 32) >= ((int64_t)1 << 31))
+        return fail(FD_ERR_ARG, "plane of %lld x %lld points too large (32-bit in-plane offsets)",
+                    (long long)nyg, (long long)nxg);
     int64_t z0 = 0, z1 = nzg;
     if (nranks > 1 || rank != 0) {
         fd_status s = partition(nzg, nranks, rank, &z0, &z1);
@@ -881,7 +890,8 @@ static fd_status prepare(fd_ctx *c) {
         // auto: small single-slab grids with no pinned tile / step mode
         const bool want = c->opt_resident == 2 ||
                           (c->nxg * c->nyg * c->nzg <= kResidentAutoPoints && c->opt_tile < 0 &&
-                           c->opt_tsteps == 0 && c->opt_vslabs == 1 && c->nranks == 1);
+                           c->opt_tsteps == 0 && c->opt_vslabs == 1 && c->nranks == 1 &&
+                           c->opt_transport == 0);
         if (want) {
             c->resident = resident_config(c);
             if (!c->resident && c->opt_resident == 2)
@@ -1346,6 +1356,24 @@ static fd_status resident_steps(fd_ctx *c, int64_t n) {
 // the neighbours' flags.  peer_wait: before launches that read halos, wait for
 // the neighbours' count of the previous exchange (which also orders our next
 // pushes after their reads of the halos those pushes overwrite).
+// Bound of a peer_wait spin (FD_PEER_TIMEOUT_S, default 60 s): a neighbour that
+// failed or died must not hang this rank's streams forever.
+static uint64_t peer_timeout_ns() {
+    static const uint64_t ns = [] {
+        const char *e = getenv("FD_PEER_TIMEOUT_S");
+        const double s = e ? atof(e) : 60.0;
+        return (uint64_t)((s > 0 ? s : 60.0) * 1e9);
+    }();
+    return ns;
+}
+static fd_status check_peer_timeout(fd_ctx *c) {
+    if (c->h_perr && *(volatile int *)c->h_perr) {
+        c->poisoned = true;
+        return fail(FD_ERR_STATE, "peer transport: a neighbour did not signal its halo exchange within %.0f s "
+                                  "(failed or exited rank); context poisoned", peer_timeout_ns() * 1e-9);
+    }
+    return FD_OK;
+}
 static void peer_signal(fd_ctx *c, cudaStream_t st) {
     ++c->xcount;
     int64_t *lo = c->rank > 0 ? c->plo.flags + 1 : nullptr;            // rank - 1 hears from its upper side
@@ -1354,7 +1382,8 @@ static void peer_signal(fd_ctx *c, cudaStream_t st) {
     ++c->launches;
 }
 static void peer_wait(fd_ctx *c, cudaStream_t st) {
-    peer_wait_kernel<<<1, 1, 0, st>>>(c->d_flags, c->rank > 0, c->rank < c->nranks - 1, c->xcount);
+    peer_wait_kernel<<<1, 1, 0, st>>>(c->d_flags, c->rank > 0, c->rank < c->nranks - 1, c->xcount, c->d_perr,
+                                      peer_timeout_ns());
     ++c->launches;
 }
 // Push `depth` boundary planes of buffer b (-1: K) into the neighbours' halos
@@ -1665,6 +1694,9 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
     if (s) return s;
     if (n < 0) return fail(FD_ERR_ARG, "n must be >= 0");
     if (n == 0) return FD_OK;
+    if (c->peer_detached) return fail(FD_ERR_STATE, "fd_step after fd_peer_detach");
+    s = check_peer_timeout(c);
+    if (s) return s;
     if (!c->started) {
         s = prepare(c);
         if (s) return s;
@@ -1733,7 +1765,11 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
     }
     s = advance_plain(c, n - i);
     if (s) return s;
-    if (!c->opt_async) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (!c->opt_async) {
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        s = check_peer_timeout(c);
+        if (s) return s;
+    }
     if (c->comm && nccl().CommGetAsyncError) {
         ncclResult_t ae = 0;
         nccl().CommGetAsyncError(c->comm, &ae);
@@ -1837,6 +1873,11 @@ fd_status fd_peer_export(fd_ctx *c, void *blob, size_t cap, size_t *len) {
         CUDA_TRY(c, cudaMemset(ss.F[b], 0, fbytes));
         c->dev_bytes += (double)fbytes;
     }
+    if (!c->h_perr) {
+        CUDA_TRY(c, cudaHostAlloc((void **)&c->h_perr, sizeof(int), cudaHostAllocMapped));
+        *c->h_perr = 0;
+        CUDA_TRY(c, cudaHostGetDevicePointer((void **)&c->d_perr, c->h_perr, 0));
+    }
     if (!c->d_flags) {
         CUDA_TRY(c, cudaMalloc(&c->d_flags, 2 * sizeof(int64_t)));
         CUDA_TRY(c, cudaMemset(c->d_flags, 0, 2 * sizeof(int64_t)));
@@ -1902,6 +1943,24 @@ fd_status fd_peer_import(fd_ctx *c, const void *lo_blob, const void *hi_blob) {
     if (lo_blob) { s = open(lo_blob, c->rank - 1, c->plo); if (s) return s; }
     if (hi_blob) { s = open(hi_blob, c->rank + 1, c->phi); if (s) return s; }
     c->peer_imported = true;
+    return FD_OK;
+}
+
+fd_status fd_peer_detach(fd_ctx *c) {
+    if (!c) return fail(FD_ERR_ARG, "context is NULL");
+    // finish every launch that may store into (or signal) the neighbours'
+    // memory, then unmap it; the caller's barrier after this call orders the
+    // neighbours' fd_destroy (which frees the exported buffers) after it
+    cudaError_t e = cudaSuccess;
+    if (c->stream) e = cudaStreamSynchronize(c->stream);
+    if (c->comm_stream && e == cudaSuccess) e = cudaStreamSynchronize(c->comm_stream);
+    for (auto *pr : {&c->plo, &c->phi}) {
+        for (void *m : pr->opened) cudaIpcCloseMemHandle(m);
+        pr->opened.clear();
+        *pr = fd_ctx::Peer{};
+    }
+    if (c->peer_imported) c->peer_detached = true;
+    CUDA_TRY(c, e);
     return FD_OK;
 }
 

@@ -90,6 +90,22 @@ def create(vel_slab: np.ndarray, global_dims, h: float, dt: float, order: int, *
     return sim
 
 
+def close(sim) -> None:
+    """Collective teardown of a slab context (every rank calls it).
+
+    Peer transport: the neighbours' last boundary stores and flag signals
+    target this rank's exported buffers, so no rank may free them while
+    another still has them mapped: synchronise and unmap (fd_peer_detach),
+    barrier, then free (fd_destroy).  NCCL transport: barrier, then free."""
+    import torch.distributed as dist
+    if sim is None or not sim.ctx:
+        return
+    _fd.fd_peer_detach(sim.ctx)
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+    sim.close()
+
+
 def all_ok(ok: bool) -> bool:
     """True iff every rank reports ok (guards collective steps after a local failure)."""
     import torch

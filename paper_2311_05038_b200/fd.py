@@ -33,7 +33,7 @@ EXPORTED = [
     "fd_set_receivers", "fd_step", "fd_get_wavefield", "fd_get_traces", "fd_destroy",
     "fd_strerror", "fd_last_error", "fd_set_stream", "fd_set_allocator", "fd_set_wavefield",
     "fd_set_option", "fd_get_info", "fd_get_kernel_times", "fd_reset_kernel_times",
-    "fd_peer_export", "fd_peer_import", "fd_set_sponge",
+    "fd_peer_export", "fd_peer_import", "fd_peer_detach", "fd_set_sponge",
 ]
 
 
@@ -103,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "fd_reset_kernel_times": ([ctypes.c_void_p], st),
         "fd_peer_export": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], st),
         "fd_peer_import": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], st),
+        "fd_peer_detach": ([ctypes.c_void_p], st),
         "fd_set_sponge": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_double], st),
     }
     for name, (args, res) in sig.items():
@@ -183,6 +184,10 @@ def fd_peer_import(ctx, lo_blob: bytes | None, hi_blob: bytes | None):
     _check(lib.fd_peer_import(ctx, lo, hi), "fd_peer_import")
 
 
+def fd_peer_detach(ctx):
+    _check(lib.fd_peer_detach(ctx), "fd_peer_detach")
+
+
 def fd_set_sponge(ctx, width: int, alpha: float = 0.015):
     _check(lib.fd_set_sponge(ctx, int(width), float(alpha)), "fd_set_sponge")
 
@@ -213,16 +218,18 @@ def fd_get_wavefield(ctx, which: int, shape, out: np.ndarray | None = None) -> n
 
 
 def fd_get_traces(ctx, nrec: int, nsteps: int, out: np.ndarray | None = None) -> np.ndarray:
-    """Receiver-major traces; ``out``: optional preallocated (e.g. pinned) float32 buffer of >= nrec*nsteps."""
+    """Receiver-major traces (nrec, steps done); ``nsteps`` sizes the buffer (>= the
+    steps done); ``out``: optional preallocated (e.g. pinned) float32 buffer of >=
+    nrec*nsteps.  The C side writes nrec rows of stride = steps done."""
     if out is None:
-        out = np.empty((nrec, nsteps), dtype=np.float32)
+        out = np.empty(nrec * nsteps, dtype=np.float32)
     else:
         if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < nrec * nsteps:
             raise ValueError("out must be a C-contiguous float32 array of >= nrec*nsteps elements")
-        out = out.reshape(-1)[: nrec * nsteps].reshape(nrec, nsteps)
+    flat = out.reshape(-1)[: nrec * nsteps]
     got = ctypes.c_int64()
-    _check(lib.fd_get_traces(ctx, out.ctypes.data_as(_f32p), out.size, ctypes.byref(got)), "fd_get_traces")
-    return out[:, : got.value] if got.value != nsteps else out
+    _check(lib.fd_get_traces(ctx, flat.ctypes.data_as(_f32p), flat.size, ctypes.byref(got)), "fd_get_traces")
+    return flat[: nrec * got.value].reshape(nrec, got.value)
 
 
 def fd_destroy(ctx):

@@ -46,7 +46,7 @@ def main():
         Pp = fdd.gather_wavefield(sim.wavefield(fd.FD_FIELD_PREV))
         T = fdd.assemble_traces(sim.traces())
         info = sim.info()
-        sim.close()
+        fdd.close(sim)
         if rank == 0:
             out[f"P{ci}"], out[f"Pp{ci}"], out[f"T{ci}"] = P, Pp, T
             out[f"spl{ci}"] = info["steps_per_launch"]

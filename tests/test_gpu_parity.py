@@ -333,7 +333,7 @@ def test_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs):
 # The paper's unfused decomposition (FD_OPT_KERNEL=3) and per-kernel profiling
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dims,order", [((30, 40, 70), 2), ((33, 28, 45), 8), ((80, 300), 4)])
-def test_unfused_decomposition_equals_fused(fd, dims, order):
+def test_unfused_decomposition_equals_fused(fd, oracle, dims, order):
     vel = _rand_vel(dims, seed=23)
     src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0)]
     recs = [tuple(d // 2 + 1 for d in dims), tuple(d // 3 for d in dims)]
@@ -348,6 +348,10 @@ def test_unfused_decomposition_equals_fused(fd, dims, order):
         info = sim.info()
     for a, b in zip(got, ref[:3]):
         assert np.array_equal(a, b)      # IEEE ==: a band term adds an exact +0
+    # and the decomposition itself against the fp64 oracle (Listing 3)
+    Po, Ppo, To = oracle.run(vel, 10.0, 1e-3, order, 25, src, recs, nthreads=4)
+    for a, b in zip(got, (Po, Ppo, To)):
+        assert rel_l2(a, b) <= TOL
     assert info["kernel"] == 3
     names = {"fd_pxx", "fd_pzz", "fd_time", "gather", "inject"} | ({"fd_pyy"} if len(dims) == 3 else set())
     assert names <= set(kt)
@@ -666,6 +670,7 @@ def _cone_case(fd, oracle, wl, k):
     assert np.linalg.norm(To[-len(near):]) > 0.5 * np.linalg.norm(To)   # the near line carries the signal
     others = np.setdiff1d(np.arange(len(wl.receivers)), inside)
     assert not T[others].any()
+    info["relL2_box"], info["relL2_traces"] = rel_l2(P[box], Po), rel_l2(T[inside], To)
     return info
 
 

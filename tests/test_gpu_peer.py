@@ -2,10 +2,13 @@
 step kernels straight into the neighbouring slab's buffers.
 
 * virtual slabs (one process): bitwise equal to one slab, single steps and
-  two steps per launch, 2D and 3D;
+  two steps per launch, 2D and 3D, and within relative L2 1e-4 of the fp64
+  oracle run in its own z-slab mode (oracle.run(nranks=...), memcpy halos);
 * two processes on the one GPU of this run (torch.distributed.run, gloo for the
   plumbing, CUDA IPC mappings + flag sync for the data path -- the multi-rank
-  code path without NCCL): bitwise equal to one process.
+  code path without NCCL): bitwise equal to one process, and the assembled
+  fields and traces within relative L2 1e-4 of the oracle (the sponge case
+  against the oracle's Cerjan run).
 """
 import os
 import subprocess
@@ -14,7 +17,7 @@ import sys
 import numpy as np
 import pytest
 
-from test_gpu_parity import _rand_vel, run_gpu
+from test_gpu_parity import TOL, _rand_vel, rel_l2, run_gpu
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -31,11 +34,18 @@ def fd():
     return m
 
 
+@pytest.fixture(scope="module")
+def oracle():
+    import oracle as o
+    o.build()
+    return o
+
+
 @pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((41, 29, 66), 4), ((45, 26, 50), 8),
                                         ((96, 300), 2), ((70, 140), 8)])
 @pytest.mark.parametrize("nslabs", [2, 3])
 @pytest.mark.parametrize("tsteps", [1, 2])
-def test_peer_virtual_slabs_bitwise(fd, dims, order, nslabs, tsteps):
+def test_peer_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs, tsteps):
     if tsteps == 2 and len(dims) == 3 and order > 4:
         pytest.skip("two-step kernel: 3D r <= 2")
     vel = _rand_vel(dims, seed=73)
@@ -53,6 +63,9 @@ def test_peer_virtual_slabs_bitwise(fd, dims, order, nslabs, tsteps):
                                fd.FD_OPT_GRAPH: graph})
         for a, b in zip(got[:3], ref[:3]):
             assert np.array_equal(a, b), (nslabs, tsteps, graph)
+    # the oracle's own slab mode (memcpy halos, bitwise its global run)
+    Po, Ppo, To = oracle.run(vel, 10.0, 5e-4, order, 33, src, recs, nranks=nslabs, nthreads=4)
+    assert rel_l2(got[0], Po) <= TOL and rel_l2(got[1], Ppo) <= TOL and rel_l2(got[2], To) <= TOL
 
 
 def test_peer_transport_needs_slabs(fd):
@@ -64,7 +77,7 @@ def test_peer_transport_needs_slabs(fd):
 
 
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
+def test_peer_two_processes_one_gpu_bitwise(fd, oracle, tmp_path, nranks):
     import importlib.util
     spec = importlib.util.spec_from_file_location("peer_worker", os.path.join(ROOT, "tests", "peer_worker.py"))
     worker = importlib.util.module_from_spec(spec)
@@ -97,6 +110,14 @@ def test_peer_two_processes_one_gpu_bitwise(fd, tmp_path, nranks):
         assert np.array_equal(got[f"P{ci}"], ref[0]), ci
         assert np.array_equal(got[f"Pp{ci}"], ref[1]), ci
         assert np.array_equal(got[f"T{ci}"], ref[2]), ci
+        # the multi-rank result against the fp64 oracle (slab mode; Cerjan frame for the sponge case)
+        steps = sum(seq)
+        if sponge:
+            Po, Ppo, To = oracle.run(vel, 10.0, 5e-4, order, steps, src, recs, sponge=sponge, nthreads=4)
+        else:
+            Po, Ppo, To = oracle.run(vel, 10.0, 5e-4, order, steps, src, recs, nranks=nranks, nthreads=4)
+        for a, b in ((got[f"P{ci}"], Po), (got[f"Pp{ci}"], Ppo), (got[f"T{ci}"], To)):
+            assert rel_l2(a, b) <= TOL, (ci, rel_l2(a, b))
 
 
 @pytest.mark.parametrize("strong", [False, True])
