@@ -328,7 +328,8 @@ def run_reference(args, wl):
             f"{cores} threads")
     line = {
         "impl": "reference", "metric": "grid-point updates/s (Gpts/s)", "value": value, "unit": "Gpts/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.name, "grid": list(wl.dims), "order": wl.order, "model": wl.model,
                    "sample_grid": list(dims_s)},
@@ -413,7 +414,7 @@ def run_ours(args, wl):
     sim.step(args.warmup)
     # setup for the timed steps (trace/wavelet tables for both passes, the CUDA
     # graphs to replay) happens here, outside the timed region
-    sim.reserve(2 * args.steps)
+    sim.reserve((args.reps + 1) * args.steps)
     stream.synchronize()
     launches0 = sim.info()["kernel_launches"]
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -421,18 +422,33 @@ def run_ours(args, wl):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    # pass 1 (the value): K steps exactly as a user runs them (CUDA-graph replay)
+    # pass 1 (the value): K steps exactly as a user runs them (CUDA-graph
+    # replay), repeated --reps times (each repetition exactly K steps between
+    # barriers + synchronize); the value is the median repetition, max over
+    # ranks per repetition (min and median of >= 5 repetitions)
     sampler = {"nvml": NvmlClockSampler, "smi": ClockSampler}.get(args.clock_sampler, NvmlClockSampler)
+    rep_ms = []
     with sampler(local) as clk:
-        ev0.record(stream)
-        sim.step(args.steps)
-        ev1.record(stream)
-        ev1.synchronize()
-    torch.cuda.synchronize()
+        for rep in range(args.reps):
+            if rep:
+                if world > 1:
+                    torch.distributed.barrier()
+                torch.cuda.synchronize()
+            ev0.record(stream)
+            sim.step(args.steps)
+            ev1.record(stream)
+            ev1.synchronize()
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            rep_ms.append(ev0.elapsed_time(ev1))
+    launches = (sim.info()["kernel_launches"] - launches0) / args.reps
     if world > 1:
-        torch.distributed.barrier()
-    ms = ev0.elapsed_time(ev1)
-    launches = sim.info()["kernel_launches"] - launches0
+        t = torch.tensor(rep_ms, dtype=torch.float64,
+                         device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        rep_ms = [float(x) for x in t.cpu().tolist()]
+    ms = float(np.median(rep_ms))
     # pass 2 (per-kernel breakdown): K more steps with CUDA events around every
     # launch on the library's stream.  At N = 1 the roofline's kernel time comes
     # from pass 1 itself (its events ÷ the step-kernel launches): the GPU runs
@@ -474,10 +490,6 @@ def run_ours(args, wl):
             sim.close()
         return out
 
-    if world > 1:
-        t = torch.tensor([ms], device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
     gpts = npts_global * args.steps / (ms / 1e3) / 1e9
 
@@ -486,7 +498,7 @@ def run_ours(args, wl):
     # back (D2H).  The input arrays exist before the clock starts.
     if args.no_e2e:
         return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, None, ktimes,
-                     sustained_pass())
+                     sustained_pass(), rep_ms)
     vel_pin = torch.empty(vel.shape, dtype=torch.float32, pin_memory=True).numpy()
     vel_pin[...] = vel
     out_pin = torch.empty(vel.shape, dtype=torch.float32, pin_memory=True).numpy()
@@ -520,7 +532,20 @@ def run_ours(args, wl):
            "seconds": e2e_s, "seconds_runs": runs, "pinned_host_buffers": True,
            "what": "fd_create (model upload) + fd_step(K) + fd_get_traces + fd_get_wavefield",
            "device_memory": "torch caching allocator (fd_set_allocator)" if args.transport != "peer" else "cudaMalloc"}
-    return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes, sustained_pass())
+    return _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes, sustained_pass(),
+                 rep_ms)
+
+
+def _reps_summary(rep_ms, wl, world, args):
+    """The timed repetitions of pass 1 (each exactly K steps; max over ranks)."""
+    if not rep_ms:
+        return None
+    npts = (1 if args.strong else world) * wl.npts
+    rate = [npts * args.steps / (m / 1e3) / 1e9 for m in rep_ms]
+    return {"n": len(rep_ms), "ms": rep_ms, "value_median": float(np.median(rate)), "value_max": max(rate),
+            "value_min": min(rate), "ms_per_step_min": min(rep_ms) / args.steps,
+            "ms_per_step_median": float(np.median(rep_ms)) / args.steps,
+            "what": "value = the median repetition; each repetition K steps between barrier + synchronize"}
 
 
 def _l2_note(wl) -> str:
@@ -532,7 +557,8 @@ def _l2_note(wl) -> str:
     return "working set %.2f MB fits the 126 MB L2 (launch/latency-bound config, not a bandwidth number)" % (ws / 1e6)
 
 
-def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes, sustained=None):
+def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e, ktimes, sustained=None,
+          rep_ms=None):
     peak, peak_src = _peaks()
     # dominant kernel: the fused step kernel, one launch per step; its average
     # launch duration from the events around each launch in the timed region
@@ -601,7 +627,10 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
                    **({"k_storage": "per-plane table (FD_OPT_KPLANE; the model is layered)" if kz else
                        "K field (per-plane table requested, model not plane-constant)"} if args.kplane else {}),
                    "global_grid": list(_global_dims(wl, world, args.strong)),
-                   "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"]},
+                   "tile": [info["tile_x"], info["tile_y"]], "zchunks": info["zchunks"], "ctas": info["ctas"],
+                   **({"nccl_comm_nranks": info.get("comm_nranks")} if world > 1 else {}),
+                   "graph_steps": info.get("graph_steps")},
+        "repetitions": _reps_summary(rep_ms, wl, world, args),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "traces_finite": finite,
         **({"sustained": sustained} if sustained else {}),
@@ -642,14 +671,75 @@ def main(argv=None):
                          "not the headline)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
+    ap.add_argument("--reps", type=int, default=5,
+                    help="repetitions of the K timed steps (value = the median repetition; min/median/max reported)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="start the N ranks (spawning torchrun when --gpus N > 1 has no WORLD_SIZE), check the "
+                         "world size, print one JSON line and exit (no GPU work; tests the launch path)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    args.reps = max(1, args.reps)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return spawn_ranks(args, sys.argv[1:] if argv is None else list(argv))
+    rank, world, _ = dist_env()
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        return 2
+    if args.launch_check:
+        return launch_check(args)
     from workloads import config
     wl = config(args.config, order=args.order)
     if args.impl == "reference":
         return run_reference(args, wl)
     return run_ours(args, wl)
+
+
+def spawn_ranks(args, argv) -> int:
+    """`bench.py --gpus N` without torchrun's environment: start N ranks on this
+    node (python -m torch.distributed.run, rendezvous on 127.0.0.1), one per GPU,
+    with NCCL's init log on (communicator rank counts in stderr).  Refuses when
+    the node has fewer than N GPUs (FD_BENCH_SHARE_GPU=1: every rank on cuda:0,
+    test hook, not a scaling number)."""
+    import socket
+    share = os.environ.get("FD_BENCH_SHARE_GPU") == "1"
+    if not share:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have} "
+                  f"(FD_BENCH_SHARE_GPU=1 runs every rank on cuda:0 as a test hook)", file=sys.stderr)
+            return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def launch_check(args) -> int:
+    """One JSON line from rank 0 after every rank joined the process group (gloo)."""
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        t = [None] * world
+        dist.all_gather_object(t, (rank, local))
+        dist.barrier()
+    else:
+        t = [(0, local)]
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "ranks": [list(x) for x in t]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":

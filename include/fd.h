@@ -281,6 +281,8 @@ typedef struct {
                                /* fd_step call is one cluster launch (FD_OPT_RESIDENT), else 1 */
     int cluster_ctas;          /* CTAs of the resident cluster (FD_OPT_RESIDENT), else 0 */
     int kplane;                /* 1 when the kernels read K per plane (FD_OPT_KPLANE)    */
+    int comm_nranks;           /* ranks of the NCCL communicator (ncclCommCount; 0: none) */
+    int64_t graph_steps;       /* steps advanced by CUDA-graph replay so far             */
 } fd_info;
 fd_status fd_get_info(fd_ctx *ctx, fd_info *out);
 

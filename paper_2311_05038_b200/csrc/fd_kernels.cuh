@@ -962,43 +962,97 @@ __global__ void naive_step_kernel(const StepParams prm) {
 //   S = (Pxx + Pyy) + Pzz  and  p_next = fma(K, S, fma(2, p, -p_prev))
 // equals the fused kernel's canonical expression (a band term contributes an
 // exact +0).  Fields are pitched like K (no halo planes).
-template <int R, int AXIS>   // AXIS 0 = x, 1 = y, 2 = z
-__global__ void d2_axis_kernel(const StepParams prm, float *__restrict__ out) {
-    const int64_t nx = prm.nx, ny = prm.ny, P = prm.pitch;
-    const int64_t npl = nx * ny, total = npl * prm.nz;
-    constexpr float c0 = tap(R, 0);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
-        const int64_t i = ((z + halo_planes(R)) * ny + y) * P + x;      // field buffer index
-        const int64_t s = AXIS == 0 ? 1 : (AXIS == 1 ? P : ny * P);
-        const int64_t ia = AXIS == 0 ? x : (AXIS == 1 ? y : prm.gz0 + z);
-        const int64_t na = AXIS == 0 ? nx : (AXIS == 1 ? ny : prm.nzg);
-        float v = 0.f;
-        if (ia >= R && ia < na - R) {
-            v = __fmul_rn(c0, prm.p[i]);
+// Launch geometry (r2): a 2D/3D grid of 32 x 8 threads, each thread a quad of
+// 4 consecutive x points of one row (float4 loads and stores, coalesced), no
+// index division; blocks run plane by plane (blockIdx.z = z in 3D), so the
+// z taps of neighbouring planes hit in L2.  3D: grid (ceil(nx/128),
+// ceil(ny/8), nz); 2D: grid (ceil(nx/128), ceil(nz/8), 1).  Roofline: 8 B per
+// point for a derivative kernel (read p, write the field), 28 B (3D) / 24 B
+// (2D) for fd_time.
+struct QuadPos {
+    int x, y, z;
+    bool ok;
+};
+template <int NDIM>
+__device__ __forceinline__ QuadPos quad_pos(const StepParams &prm) {
+    QuadPos q;
+    q.x = (blockIdx.x * 32 + threadIdx.x) * 4;
+    if (NDIM == 3) { q.y = blockIdx.y * 8 + threadIdx.y; q.z = blockIdx.z; }
+    else { q.y = 0; q.z = blockIdx.y * 8 + threadIdx.y; }
+    q.ok = q.x < (int)prm.nx && q.y < (int)prm.ny && q.z < prm.nz;
+    return q;
+}
+// store the in-grid elements of a quad (the pitch padding is never written)
+__device__ __forceinline__ void st_quad(float *dst, const float4 v, int x, int nx) {
+    if (x + 3 < nx) { *reinterpret_cast<float4 *>(dst) = v; return; }
 #pragma unroll
-            for (int m = 1; m <= R; ++m) v = __fmaf_rn(tap(R, m), __fadd_rn(prm.p[i - m * s], prm.p[i + m * s]), v);
+    for (int e = 0; e < 4; ++e)
+        if (x + e < nx) dst[e] = f4(v, e);
+}
+
+template <int R, int AXIS, int NDIM>   // AXIS 0 = x, 1 = y, 2 = z
+__global__ void __launch_bounds__(256) d2_axis_kernel(const StepParams prm, float *__restrict__ out) {
+    const QuadPos q = quad_pos<NDIM>(prm);
+    if (!q.ok) return;
+    const int nx = (int)prm.nx, ny = (int)prm.ny;
+    const int64_t P = prm.pitch;
+    const int64_t i = ((int64_t)(q.z + halo_planes(R)) * ny + q.y) * P + q.x;   // field buffer index
+    const float *p = prm.p;
+    constexpr float c0 = tap(R, 0);
+    const float4 M = lds128(p + i);       // generic float4 load (global)
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (AXIS == 0) {
+        const float4 L = lds128(p + i - 4), Rt = lds128(p + i + 4);
+        const float a[12] = {L.x, L.y, L.z, L.w, M.x, M.y, M.z, M.w, Rt.x, Rt.y, Rt.z, Rt.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float d = __fmul_rn(c0, a[4 + e]);
+#pragma unroll
+            for (int m = 1; m <= R; ++m) d = __fmaf_rn(tap(R, m), __fadd_rn(a[4 + e - m], a[4 + e + m]), d);
+            f4set(v, e, (q.x + e >= R && q.x + e < nx - R) ? d : 0.f);
         }
-        out[(z * ny + y) * P + x] = v;
+    } else {
+        const int64_t st = AXIS == 1 ? P : (int64_t)ny * P;
+        const int ia = AXIS == 1 ? q.y : (int)prm.gz0 + q.z;
+        const int na = AXIS == 1 ? ny : (int)prm.nzg;
+        if (ia >= R && ia < na - R) {
+            float4 lo[R], hi[R];
+#pragma unroll
+            for (int m = 1; m <= R; ++m) { lo[m - 1] = lds128(p + i - m * st); hi[m - 1] = lds128(p + i + m * st); }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float d = __fmul_rn(c0, f4(M, e));
+#pragma unroll
+                for (int m = 1; m <= R; ++m) d = __fmaf_rn(tap(R, m), __fadd_rn(f4(lo[m - 1], e), f4(hi[m - 1], e)), d);
+                f4set(v, e, d);
+            }
+        }
     }
+    st_quad(out + ((int64_t)q.z * ny + q.y) * P + q.x, v, q.x, nx);
 }
 
 template <int R, int NDIM>
-__global__ void time_update_kernel(const StepParams prm, const float *__restrict__ pxx,
-                                   const float *__restrict__ pyy, const float *__restrict__ pzz) {
-    const int64_t nx = prm.nx, ny = prm.ny, P = prm.pitch;
-    const int64_t npl = nx * ny, total = npl * prm.nz;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = t / npl, rem = t % npl, y = rem / nx, x = rem % nx;
-        const int64_t ik = (z * ny + y) * P + x;
-        const int64_t i = ((z + halo_planes(R)) * ny + y) * P + x;
-        float S = pxx[ik];
-        if (NDIM == 3) S = __fadd_rn(S, pyy[ik]);
-        S = __fadd_rn(S, pzz[ik]);
-        prm.pnext[i] = time_update_rt(prm, prm.K[ik], S, prm.p[i], prm.pnext[i], (int)(prm.gz0 + z), (int)y, (int)x);
+__global__ void __launch_bounds__(256) time_update_kernel(const StepParams prm, const float *__restrict__ pxx,
+                                                          const float *__restrict__ pyy,
+                                                          const float *__restrict__ pzz) {
+    const QuadPos q = quad_pos<NDIM>(prm);
+    if (!q.ok) return;
+    const int nx = (int)prm.nx, ny = (int)prm.ny;
+    const int64_t P = prm.pitch;
+    const int64_t ik = ((int64_t)q.z * ny + q.y) * P + q.x;
+    const int64_t i = ((int64_t)(q.z + halo_planes(R)) * ny + q.y) * P + q.x;
+    const float4 dx = lds128(pxx + ik), dz = lds128(pzz + ik), k4 = lds128(prm.K + ik);
+    const float4 dy = NDIM == 3 ? lds128(pyy + ik) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 pc = lds128(prm.p + i), pp = lds128(prm.pnext + i);
+    float4 o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        float S = f4(dx, e);
+        if (NDIM == 3) S = __fadd_rn(S, f4(dy, e));
+        S = __fadd_rn(S, f4(dz, e));
+        f4set(o, e, time_update_rt(prm, f4(k4, e), S, f4(pc, e), f4(pp, e), (int)prm.gz0 + q.z, q.y, q.x + e));
     }
+    st_quad(prm.pnext + i, o, q.x, nx);
 }
 
 // receivers of the naive path: trace_row[id] = p_next at (z, y, x) (raw, before injection)

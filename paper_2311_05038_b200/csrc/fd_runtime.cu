@@ -138,6 +138,7 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -157,6 +158,7 @@ static NcclApi &nccl() {
             NCCL_SYM(CommInitRank, "ncclCommInitRank");
             NCCL_SYM(CommDestroy, "ncclCommDestroy");
             NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+            NCCL_SYM(CommCount, "ncclCommCount");
             NCCL_SYM(Send, "ncclSend");
             NCCL_SYM(Recv, "ncclRecv");
             NCCL_SYM(GroupStart, "ncclGroupStart");
@@ -232,6 +234,7 @@ struct fd_ctx {
     float *d_wtab = nullptr;              // [wcap][nsrc]: w_j of source s (fp32 of the fp64 Ricker)
     int64_t wcap = 0;
     int64_t *d_k = nullptr;               // device step counter (graph replays)
+    int64_t graph_steps = 0;              // steps advanced by graph replay (fd_get_info)
     cudaStream_t own_stream = nullptr;    // used when no stream was set (capturable)
     // CUDA graphs of G steps (one per starting buffer parity), re-captured when
     // the trace / wavelet tables move
@@ -1173,14 +1176,18 @@ static void dispatch_inject(fd_ctx *c, cudaStream_t st, float *field, const Step
 
 template <int R, int NDIM>
 static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStream_t st, const StepParams &p) {
-    const int64_t total = c->nxg * c->nyg * s.nz;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    // 32 x 8 threads, one quad of x points each; plane-major blocks (fd_kernels.cuh)
+    const unsigned gx = (unsigned)((c->nxg + 127) / 128);
+    const dim3 grid = NDIM == 3 ? dim3(gx, (unsigned)((c->nyg + 7) / 8), (unsigned)s.nz)
+                                : dim3(gx, (unsigned)((s.nz + 7) / 8), 1u);
+    const dim3 blk(32, 8);
     // Listing 3 order: fd_pzz, [fd_pyy], fd_pxx, fd_time
-    tracked(cm, FD_K_PZZ, st, [&] { d2_axis_kernel<R, 2><<<blocks, 256, 0, st>>>(p, s.D[2]); });
-    if (NDIM == 3) tracked(cm, FD_K_PYY, st, [&] { d2_axis_kernel<R, 1><<<blocks, 256, 0, st>>>(p, s.D[1]); });
-    tracked(cm, FD_K_PXX, st, [&] { d2_axis_kernel<R, 0><<<blocks, 256, 0, st>>>(p, s.D[0]); });
+    tracked(cm, FD_K_PZZ, st, [&] { d2_axis_kernel<R, 2, NDIM><<<grid, blk, 0, st>>>(p, s.D[2]); });
+    if (NDIM == 3)
+        tracked(cm, FD_K_PYY, st, [&] { d2_axis_kernel<R, 1, NDIM><<<grid, blk, 0, st>>>(p, s.D[1]); });
+    tracked(cm, FD_K_PXX, st, [&] { d2_axis_kernel<R, 0, NDIM><<<grid, blk, 0, st>>>(p, s.D[0]); });
     tracked(cm, FD_K_TIME, st,
-            [&] { time_update_kernel<R, NDIM><<<blocks, 256, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });
+            [&] { time_update_kernel<R, NDIM><<<grid, blk, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });
 }
 
 // In-kernel halo pushes of a boundary launch (FD_OPT_TRANSPORT = 1): buffer b1
@@ -1525,12 +1532,20 @@ static fd_status advance_plain(fd_ctx *c, int64_t m) {
 // ------------------------------------------------------------ CUDA graphs
 // kGraphSteps consecutive steps captured once per starting buffer parity and
 // replayed (launch-bound small grids).  Kernels read k = *d_k + offset; the
-// graph ends by advancing d_k.  Not used across NCCL ranks or while profiling.
+// graph ends by advancing d_k.  Not used while profiling, nor with the peer
+// transport across ranks (its flag waits carry per-exchange counts).
 constexpr int64_t kGraphSteps = 16;
 
 static bool graphs_usable(const fd_ctx *c) {
-    // virtual slabs: the two-stream schedule is captured too (event fork/join)
-    return c->opt_graph && c->nranks == 1 && !c->opt_profile && c->d_k && c->stream && !c->resident;
+    // virtual slabs: the two-stream schedule is captured too (event fork/join).
+    // NCCL ranks: the send/recv of the halo exchange are captured with the
+    // kernels (NCCL supports stream capture); only after the first plain step,
+    // so that NCCL's lazy connection setup has happened outside any capture.
+    // Every rank replays the same sequence (the graph choice depends on the
+    // buffer roles and the step count only), so the captured sends and
+    // receives pair up as the plain ones do.
+    const bool ranks_ok = c->nranks == 1 || (c->opt_transport == 0 && c->comm && c->injected && c->k > 0);
+    return c->opt_graph && ranks_ok && !c->opt_profile && c->d_k && c->stream && !c->resident;
 }
 
 // Capture kGraphSteps steps starting from the current buffer roles; the
@@ -1758,6 +1773,7 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
             auto &g = c->graphs[gi];
             CUDA_TRY(c, cudaGraphLaunch(g.exec, c->stream));
             c->k += kGraphSteps;
+            c->graph_steps += kGraphSteps;
             c->icur = g.end_icur;
             c->iprev = g.end_iprev;
             c->launches += g.launches;
@@ -2128,6 +2144,11 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->device_bytes = c->dev_bytes;
     o->steps_per_launch = (c->opt_tsteps == 2) ? 2 : 1;
     o->kplane = c->kplane ? 1 : 0;
+    o->graph_steps = c->graph_steps;
+    if (c->comm && nccl().CommCount) {
+        int n = 0;
+        if (nccl().CommCount(c->comm, &n) == 0) o->comm_nranks = n;
+    }
     if (c->opt_kernel != 0) { o->kernel = c->opt_kernel; return FD_OK; }
     o->kernel = 2;
     if (c->resident) {

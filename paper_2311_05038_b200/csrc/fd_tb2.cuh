@@ -49,6 +49,40 @@ __device__ __forceinline__ void role_release(B *...bars) {
 #endif
 }
 
+// x taps of a thread's quad: av[0..3] = the left quad, av[4..7] = M4 (the
+// thread's own 4 points), av[8..11] = the right quad; only av[4-R..3] and
+// av[8..7+R] are read.  For R <= 2 the halo values are the neighbouring lanes'
+// own quads (lane - 1 / lane + 1 own x - 4 .. x - 1 / x + 4 .. x + 7): taken by
+// warp shuffles, and from shared memory (`lq` = the left quad's address, the
+// right quad at lq + 8) only by the lanes whose neighbour in x is not the
+// adjacent lane (needL / needR: warp edge or row-group edge).  The scalar
+// halo loads they replace read 4 B at a 16 B lane stride -- 4-way bank
+// conflicts, 76 % of the excess shared wavefronts of the r05f profile.  Every
+// lane of the warp must execute this (full-mask shuffles).
+template <int R>
+__device__ __forceinline__ void quad_xtaps(float (&av)[12], const float4 M4, const float *lq, bool needL, bool needR) {
+    av[4] = M4.x; av[5] = M4.y; av[6] = M4.z; av[7] = M4.w;
+    if constexpr (R <= 2) {
+#pragma unroll
+        for (int m = 1; m <= R; ++m) {
+            av[4 - m] = __shfl_up_sync(0xffffffffu, f4(M4, 4 - m), 1);
+            av[7 + m] = __shfl_down_sync(0xffffffffu, f4(M4, m - 1), 1);
+        }
+        if (needL) {
+            const float4 L4 = lds128(lq);
+            av[0] = L4.x; av[1] = L4.y; av[2] = L4.z; av[3] = L4.w;
+        }
+        if (needR) {
+            const float4 R4 = lds128(lq + 8);
+            av[8] = R4.x; av[9] = R4.y; av[10] = R4.z; av[11] = R4.w;
+        }
+    } else {
+        const float4 L4 = lds128(lq), R4 = lds128(lq + 8);
+        av[0] = L4.x; av[1] = L4.y; av[2] = L4.z; av[3] = L4.w;
+        av[8] = R4.x; av[9] = R4.y; av[10] = R4.z; av[11] = R4.w;
+    }
+}
+
 // ------------------------------------------------------------------ warp-specialised variant
 // Same two-step pass, but stage A and stage B run on separate warp groups that
 // overlap (no CTA barrier per plane) and both keep their z taps in a register
@@ -176,6 +210,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
 #pragma unroll
         for (int yy = 0; yy < C::NYA; ++yy) sgy[yy] = SP ? sponge_gy(prm, y0 - R + re0 + yy) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
+        const bool needL = lane == 0 || q == 0, needR = lane == 31 || q == C::QXE - 1;
         // per row: band rule along y, stored to C (tile interior), offset in a plane
         uint32_t ymask = 0, stmask = 0;
         int roff[C::NYA];
@@ -232,16 +267,17 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (act) {
-                float4 col[C::NYA + 2 * R];
+            {   // all lanes (inactive ones compute on row 0 / quad 0 and store nothing): the x taps shuffle
+                float4 col[C::NYA + 2 * R];       // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
-                for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
+                for (int i = 0; i < C::NYA + 2 * R; ++i)
+                    col[i] = (i >= R && i < R + C::NYA) ? qz[(PH + R) % Q][i - R]
+                                                        : lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
                     const int re = re0 + yy;
-                    const float *row = tc + (re + R) * C::BX0 + 4 * q;
-                    const float4 L4 = lds128(row), M4 = qz[(PH + R) % Q][yy], R4 = lds128(row + 8);
-                    const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                    float av[12];
+                    quad_xtaps<R>(av, qz[(PH + R) % Q][yy], tc + (re + R) * C::BX0 + 4 * q, needL, needR);
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kza) : lds128(tk + offe);
                     const bool iny = (ymask >> yy) & 1u;
@@ -275,7 +311,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                             f4set(o, dx, __fadd_rn(f4(o, dx), wv[s2]));
                         }
                     }
-                    *reinterpret_cast<float4 *>(t1 + offe) = o;
+                    if (act) *reinterpret_cast<float4 *>(t1 + offe) = o;
                     if (store && ((stmask >> yy) & 1u)) {
                         *reinterpret_cast<float4 *>(cpl + roff[yy]) = o;
                         if (push1) peer_store4<R>(prm.peer1, z1, (int)prm.nz, plane, (int64_t)roff[yy], o);
@@ -322,6 +358,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
     const bool act = tb < C::NTB;
     const int qi = act ? tb % C::QXI : 0, ri0 = act ? (tb / C::QXI) * C::NYB : 0;
     const int q = qi + 1, xb = x0 + 4 * qi;
+    const bool needL = lane == 0 || qi == 0, needR = lane == 31 || qi == C::QXI - 1;
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
@@ -384,16 +421,18 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
         const float kzb = KZ ? kplane(prm, z2) : 0.f;
         float4 out[C::NYB];
-        if (act) {
-            float4 col[C::NYB + 2 * R];
+        {   // all lanes (inactive ones compute on row 0 and store nothing): the x taps shuffle
+            float4 col[C::NYB + 2 * R];           // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
-            for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
+            for (int i = 0; i < C::NYB + 2 * R; ++i)
+                col[i] = (i >= R && i < R + C::NYB) ? qz[(PH + R) % Q][i - R]
+                                                    : lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy) {
                 const int re = ri0 + yy + R;
                 const int offe = re * C::BXE + 4 * q;
-                const float4 L4 = lds128(t1c + offe - 4), M4 = qz[(PH + R) % Q][yy], R4 = lds128(t1c + offe + 4);
-                const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                float av[12];
+                quad_xtaps<R>(av, qz[(PH + R) % Q][yy], t1c + offe - 4, needL, needR);
                 const float4 pk4 = lds128(tpk + (re + R) * C::BX0 + 4 * q + 4);
                 const float4 k4 = KZ ? splat4(kzb) : lds128(tk + offe);
                 const bool iny = (ymask >> yy) & 1u;
@@ -569,6 +608,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
 #pragma unroll
         for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
+        const bool needL = lane == 0 || q == 0, needR = lane == 31 || q == C::QXE - 1;
         uint32_t smask = 0;
         for (int s2 = 0; s2 < prm.nsrc; ++s2)
             if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
@@ -584,16 +624,15 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             float4 oraw[C::NYA];                                   // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (act) {
+            {   // all lanes (inactive ones compute on row 0 / quad 0 and store nothing): the x taps shuffle
                 float4 col[C::NYA + 2 * R];
 #pragma unroll
                 for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tp + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
                     const int re = re0 + yy, z = rb - R + re;
-                    const float *row = tp + (re + R) * C::BX0 + 4 * q;
-                    const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
-                    const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                    float av[12];
+                    quad_xtaps<R>(av, col[yy + R], tp + (re + R) * C::BX0 + 4 * q, needL, needR);
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kplane(prm, z)) : lds128(tk + offe);
                     const int gz = (int)prm.gz0 + z;
@@ -623,8 +662,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                             f4set(o, dx, __fadd_rn(f4(o, dx), wv[s2]));
                         }
                     }
-                    *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (interior && xb < (int)prm.pitch) {
+                    if (act) *reinterpret_cast<float4 *>(t1 + offe) = o;
+                    if (act && interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + halo_planes(R)) * prm.pitch + xb) = o;
                         if (anyp) peer_store4<R>(prm.peer1, z, (int)prm.nz, prm.pitch, xb, o);
                     }
@@ -649,6 +688,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const bool act = tb < C::NTB;
     const int qi = act ? tb % C::QXI : 0, ri0 = act ? (tb / C::QXI) * C::NYB : 0;
     const int q = qi + 1, xb = x0 + 4 * qi;
+    const bool needL = lane == 0 || qi == 0, needR = lane == 31 || qi == C::QXI - 1;
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
@@ -668,7 +708,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         const float *t1 = sP1 + s1 * C::EF;
         const int zt = rb + ri0;
         float4 out[C::NYB];
-        if (act) {
+        {   // all lanes (inactive ones compute on row 0 and store nothing): the x taps shuffle
             float4 col[C::NYB + 2 * R];
 #pragma unroll
             for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1 + (ri0 + i) * C::BXE + 4 * q);
@@ -676,8 +716,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             for (int yy = 0; yy < C::NYB; ++yy) {
                 const int re = ri0 + yy + R;
                 const int offe = re * C::BXE + 4 * q;
-                const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
-                const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
+                float av[12];
+                quad_xtaps<R>(av, col[yy + R], t1 + offe - 4, needL, needR);
                 const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4);
                 const float4 k4 = KZ ? splat4(kplane(prm, zt + yy)) : lds128(tk + offe);
                 const int gz = (int)prm.gz0 + zt + yy;

@@ -57,7 +57,8 @@ class FdInfo(ctypes.Structure):
                 ("k_stages", ctypes.c_int), ("ctas", ctypes.c_int), ("threads_per_cta", ctypes.c_int),
                 ("smem_bytes", ctypes.c_int), ("zchunks", ctypes.c_int), ("order", ctypes.c_int),
                 ("device_bytes", ctypes.c_double), ("steps_per_launch", ctypes.c_int),
-                ("cluster_ctas", ctypes.c_int), ("kplane", ctypes.c_int)]
+                ("cluster_ctas", ctypes.c_int), ("kplane", ctypes.c_int), ("comm_nranks", ctypes.c_int),
+                ("graph_steps", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {}

@@ -58,3 +58,35 @@ def test_our_arm_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     s = d["sustained"]
     assert s["value"] > 0 and s["steps"] >= 40
+
+
+def test_gpus_flag_spawns_ranks_launch_check():
+    """`bench.py --gpus 2` without torchrun's environment starts two ranks
+    itself (torch.distributed.run on 127.0.0.1) and rank 0 reports n_gpus 2
+    (FD_BENCH_SHARE_GPU=1: no GPU count check; gloo, no GPU work)."""
+    env = {**os.environ, "FD_BENCH_SHARE_GPU": "1"}
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_requested"] == 2 and sorted(r[0] for r in d["ranks"]) == [0, 1]
+
+
+def test_gpus_flag_refuses_without_enough_gpus():
+    """Without the test hook, --gpus N on a node with fewer GPUs fails loudly
+    instead of silently measuring one GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("FD_BENCH_SHARE_GPU", "WORLD_SIZE")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 2 and "needs 2 GPUs" in p.stderr
+
+
+def test_world_size_must_match_gpus_flag():
+    env = {**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"}
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--launch-check"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 2 and "WORLD_SIZE=1" in p.stderr
