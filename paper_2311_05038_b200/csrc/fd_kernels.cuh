@@ -1031,6 +1031,70 @@ __global__ void __launch_bounds__(256) d2_axis_kernel(const StepParams prm, floa
     st_quad(out + ((int64_t)q.z * ny + q.y) * P + q.x, v, q.x, nx);
 }
 
+// fd_pzz / fd_pyy (axes with a row or plane stride): each warp owns 128
+// consecutive x points (a quad per lane) at one row/plane of the other axis and
+// streams ZB points along the derivative's axis with a register window of 2r+1
+// float4, so every input row/plane is loaded once per warp plus 2r halo loads
+// per ZB outputs (the one-point-per-thread form re-read 2r+1 rows/planes per
+// output from L2: 59-62 % of the roof at order 8, profiles/fig5_r2c.md).
+// Same arithmetic order as d2_axis_kernel (bitwise).  Grids:
+//   3D z: (ceil(nx/128), ceil(ny/8), ceil(nz/ZB))   warp -> y
+//   3D y: (ceil(nx/128), ceil(ny/ZB), ceil(nz/8))   warp -> z
+//   2D z: (ceil(nx/1024), ceil(nz/ZB), 1)           warp -> 128-point x segment
+template <int R, int AXIS, int NDIM, int ZB>
+__global__ void __launch_bounds__(256) d2_stream_kernel(const StepParams prm, float *__restrict__ out) {
+    static_assert(AXIS == 1 || AXIS == 2, "strided axes");
+    const int lane = threadIdx.x, w = threadIdx.y;
+    const int nx = (int)prm.nx, ny = (int)prm.ny, nz = (int)prm.nz;
+    const int64_t P = prm.pitch;
+    constexpr int H = halo_planes(R);
+    int x, a0, n;
+    int64_t b0, st, o0, ost;
+    if constexpr (NDIM == 2) {
+        x = (blockIdx.x * 8 + w) * 128 + 4 * lane;
+        a0 = blockIdx.y * ZB; n = nz;
+        b0 = (int64_t)H * P + x; st = P; o0 = x; ost = P;
+    } else if constexpr (AXIS == 2) {
+        x = blockIdx.x * 128 + 4 * lane;
+        const int y = blockIdx.y * 8 + w;
+        if (y >= ny) return;
+        a0 = blockIdx.z * ZB; n = nz;
+        b0 = ((int64_t)H * ny + y) * P + x; st = (int64_t)ny * P; o0 = (int64_t)y * P + x; ost = st;
+    } else {
+        x = blockIdx.x * 128 + 4 * lane;
+        const int z = blockIdx.z * 8 + w;
+        if (z >= nz) return;
+        a0 = blockIdx.y * ZB; n = ny;
+        b0 = (int64_t)(z + H) * ny * P + x; st = P; o0 = (int64_t)z * ny * P + x; ost = P;
+    }
+    if (x >= nx || a0 >= n) return;
+    const int ia0 = AXIS == 2 ? (int)prm.gz0 : 0, na = AXIS == 2 ? (int)prm.nzg : ny;
+    const float *p = prm.p + b0;
+    constexpr float c0 = tap(R, 0);
+    float4 q[2 * R + 1];
+#pragma unroll
+    for (int j = 0; j < 2 * R; ++j) q[j] = lds128(p + (int64_t)(a0 - R + j) * st);
+#pragma unroll
+    for (int t = 0; t < ZB; ++t) {
+        const int a = a0 + t;
+        if (a >= n) break;
+        q[2 * R] = lds128(p + (int64_t)(a + R) * st);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ia0 + a >= R && ia0 + a < na - R) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float d = __fmul_rn(c0, f4(q[R], e));
+#pragma unroll
+                for (int m = 1; m <= R; ++m) d = __fmaf_rn(tap(R, m), __fadd_rn(f4(q[R - m], e), f4(q[R + m], e)), d);
+                f4set(v, e, d);
+            }
+        }
+        st_quad(out + o0 + (int64_t)a * ost, v, x, nx);
+#pragma unroll
+        for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];
+    }
+}
+
 template <int R, int NDIM>
 __global__ void __launch_bounds__(256) time_update_kernel(const StepParams prm, const float *__restrict__ pxx,
                                                           const float *__restrict__ pyy,

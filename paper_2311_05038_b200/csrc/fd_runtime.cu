@@ -392,13 +392,57 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kde
         const int blocks = (int)std::min<int64_t>((rows * c->nxg + 255) / 256, 148 * 32);
         velocity_to_K_kernel<<<blocks, 256>>>(s.K, rows, c->nxg, c->pitch, c->dt, c->h, scale_of(c->R));
         CUDA_TRY(c, cudaGetLastError());
-    } else {
+    } else if (kdevh) {
         CUDA_TRY(c, cudaMemcpy(s.Kh, kdevh, kbytes, cudaMemcpyDeviceToDevice));
+    } else {
+        CUDA_TRY(c, cudaMemset(s.Kh, 0, kbytes));      // K uploaded by the caller (create_impl)
     }
     CUDA_TRY(c, cudaMemset(s.F[0], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.F[1], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.d_src_raw, 0, kMaxSources * 4));
     return FD_OK;
+}
+
+// Host validation of velocities (R#7/R#8 inputs): returns the index of the
+// first entry that is not finite and > 0 (-1 if none) and the max.  Threaded;
+// blocks of 4096 with a branch-free (vectorisable) body, the failing entry
+// located only inside a failing block.
+static int64_t scan_velocity(const float *v, int64_t n, double *vmax_out) {
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
+    nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, n / (1 << 20) + 1));
+    std::vector<float> vm((size_t)nt, 0.f);
+    std::vector<int64_t> bad((size_t)nt, -1);
+    auto work = [&](int t) {
+        const int64_t a = n * t / nt, b = n * (t + 1) / nt;
+        float m = 0.f;
+        for (int64_t i0 = a; i0 < b; i0 += 4096) {
+            const int64_t i1 = std::min<int64_t>(b, i0 + 4096);
+            int ok = 1;
+            float bm = 0.f;
+            for (int64_t i = i0; i < i1; ++i) {
+                const float x = v[i];
+                ok &= (x > 0.f) & (x <= 3.402823466e38f);     // > 0, not NaN, not +inf
+                bm = x > bm ? x : bm;
+            }
+            if (!ok) {
+                for (int64_t i = i0; i < i1; ++i)
+                    if (!(v[i] > 0.f) || !std::isfinite(v[i])) { bad[t] = i; return; }
+            }
+            m = std::max(m, bm);
+        }
+        vm[t] = m;
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto &x : th) x.join();
+    double vmax = 0;
+    for (int t = 0; t < nt; ++t) {
+        if (bad[t] >= 0) return bad[t];
+        vmax = std::max(vmax, (double)vm[t]);
+    }
+    *vmax_out = vmax;
+    return -1;
 }
 
 static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double h, double dt, int order,
@@ -435,53 +479,26 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     const int64_t plane = nyg * nxg;
     const float *vloc = vel + (vel_is_slab ? 0 : z0 * plane);
     const int64_t nloc = nz * plane;
-    // validate velocity and the CFL condition (R#8) on host metadata first
-    double vmax = 0;
-    {
-        // threaded scan: max(v) and the first invalid entry
-        int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
-        nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, nloc / (1 << 20) + 1));
-        std::vector<float> vm((size_t)nt, 0.f);
-        std::vector<int64_t> bad((size_t)nt, -1);
-        std::vector<std::thread> th;
-        for (int t = 0; t < nt; ++t)
-            th.emplace_back([&, t] {
-                const int64_t a = nloc * t / nt, b = nloc * (t + 1) / nt;
-                float m = 0.f;
-                // blocks of 4096 with a branch-free (vectorisable) body; the
-                // first invalid entry is located only in a failing block
-                for (int64_t i0 = a; i0 < b; i0 += 4096) {
-                    const int64_t i1 = std::min<int64_t>(b, i0 + 4096);
-                    int ok = 1;
-                    float bm = 0.f;
-                    for (int64_t i = i0; i < i1; ++i) {
-                        const float v = vloc[i];
-                        ok &= (v > 0.f) & (v <= 3.402823466e38f);     // > 0, not NaN, not +inf
-                        bm = v > bm ? v : bm;
-                    }
-                    if (!ok) {
-                        for (int64_t i = i0; i < i1; ++i)
-                            if (!(vloc[i] > 0.f) || !std::isfinite(vloc[i])) { bad[t] = i; return; }
-                    }
-                    m = std::max(m, bm);
-                }
-                vm[t] = m;
-            });
-        for (auto &x : th) x.join();
-        for (int t = 0; t < nt; ++t)
-            if (bad[t] >= 0)
-                return fail(FD_ERR_ARG, "velocity[%lld] = %g is not finite and > 0", (long long)bad[t],
-                            (double)vloc[bad[t]]);
-        for (int t = 0; t < nt; ++t) vmax = std::max(vmax, (double)vm[t]);
-    }
-    const double ratio = vmax * dt / h, lim = cfl_limit(ndim, R);
-    if (!(flags & FD_FLAG_ALLOW_UNSTABLE) && ratio > lim)
-        return fail(FD_ERR_UNSTABLE, "unstable: max(v)*dt/h = %.6f exceeds the CFL limit %.6f (ratio %.4f)", ratio,
-                    lim, ratio / lim);
-
+    const double lim = cfl_limit(ndim, R);
+    auto cfl_fail = [&](double vmax) -> fd_status {
+        const double ratio = vmax * dt / h;
+        if (!(flags & FD_FLAG_ALLOW_UNSTABLE) && ratio > lim)
+            return fail(FD_ERR_UNSTABLE, "unstable: max(v)*dt/h = %.6f exceeds the CFL limit %.6f (ratio %.4f)",
+                        ratio, lim, ratio / lim);
+        return FD_OK;
+    };
+    auto bad_fail = [&](int64_t i) {
+        return fail(FD_ERR_ARG, "velocity[%lld] = %g is not finite and > 0", (long long)i, (double)vloc[i]);
+    };
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        // no device: the host validation still decides the error class
         cudaGetLastError();
+        double vmax = 0;
+        const int64_t bad = scan_velocity(vloc, nloc, &vmax);
+        if (bad >= 0) return bad_fail(bad);
+        fd_status s = cfl_fail(vmax);
+        if (s) return s;
         return fail(FD_ERR_CUDA, "no CUDA device available");
     }
     if (device >= 0) {
@@ -503,10 +520,41 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     c->slabs.resize(1);
     Slab &s = c->slabs[0];
     s.z0 = z0; s.z1 = z1; s.nz = nz;
-    fd_status st = build_slab(c, s, vloc);
+    fd_status st = build_slab(c, s, nullptr, nullptr);
     if (st == FD_OK) {
-        cudaError_t e = cudaDeviceSynchronize();
+        // Pipelined model upload (P:119 copy-in): validate a chunk of planes on
+        // the host (finite, > 0, running max for the CFL check of R#8) while the
+        // previous chunk's H2D copy and K conversion run on the device; an
+        // invalid model frees everything and reports as before.
+        cudaStream_t up = nullptr;
+        cudaError_t e = cudaStreamCreate(&up);   // blocking: ordered after build_slab's memsets
+        const int64_t pf = plane_floats(c);
+        const int64_t cz = std::max<int64_t>(1, ((int64_t)32 << 20) / std::max<int64_t>(1, plane * 4));
+        double vmax = 0;
+        int64_t bad = -1;
+        for (int64_t za = 0; za < nz && e == cudaSuccess; za += cz) {
+            const int64_t zb = std::min(nz, za + cz);
+            double vm = 0;
+            const int64_t b = scan_velocity(vloc + za * plane, (zb - za) * plane, &vm);
+            if (b >= 0) { bad = za * plane + b; break; }
+            vmax = std::max(vmax, vm);
+            e = cudaMemcpy2DAsync(s.K + za * pf, c->pitch * 4, vloc + za * plane, nxg * 4, nxg * 4, nyg * (zb - za),
+                                  cudaMemcpyHostToDevice, up);
+            if (e != cudaSuccess) break;
+            const int64_t rows = nyg * (zb - za);
+            const int blocks = (int)std::min<int64_t>((rows * nxg + 255) / 256, 148 * 32);
+            velocity_to_K_kernel<<<blocks, 256, 0, up>>>(s.K + za * pf, rows, nxg, c->pitch, dt, h, scale_of(R));
+            e = cudaGetLastError();
+        }
+        if (up) {
+            const cudaError_t e2 = cudaStreamSynchronize(up);
+            if (e == cudaSuccess) e = e2;
+            cudaStreamDestroy(up);
+        }
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) st = fail(FD_ERR_CUDA, "device setup failed: %s", cudaGetErrorString(e));
+        else if (bad >= 0) st = bad_fail(bad);
+        else st = cfl_fail(vmax);
     }
     if (st != FD_OK) {
         destroy_all(c);
@@ -1181,10 +1229,16 @@ static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStrea
     const dim3 grid = NDIM == 3 ? dim3(gx, (unsigned)((c->nyg + 7) / 8), (unsigned)s.nz)
                                 : dim3(gx, (unsigned)((s.nz + 7) / 8), 1u);
     const dim3 blk(32, 8);
+    // fd_pzz / fd_pyy stream ZB points along their axis per thread
+    constexpr int ZB = 32;
+    const unsigned nzb = (unsigned)((s.nz + ZB - 1) / ZB);
+    const dim3 gz = NDIM == 3 ? dim3(gx, (unsigned)((c->nyg + 7) / 8), nzb)
+                              : dim3((unsigned)((c->nxg + 1023) / 1024), nzb, 1u);
+    const dim3 gy(gx, (unsigned)((c->nyg + ZB - 1) / ZB), (unsigned)((s.nz + 7) / 8));
     // Listing 3 order: fd_pzz, [fd_pyy], fd_pxx, fd_time
-    tracked(cm, FD_K_PZZ, st, [&] { d2_axis_kernel<R, 2, NDIM><<<grid, blk, 0, st>>>(p, s.D[2]); });
+    tracked(cm, FD_K_PZZ, st, [&] { d2_stream_kernel<R, 2, NDIM, ZB><<<gz, blk, 0, st>>>(p, s.D[2]); });
     if (NDIM == 3)
-        tracked(cm, FD_K_PYY, st, [&] { d2_axis_kernel<R, 1, NDIM><<<grid, blk, 0, st>>>(p, s.D[1]); });
+        tracked(cm, FD_K_PYY, st, [&] { d2_stream_kernel<R, 1, NDIM, ZB><<<gy, blk, 0, st>>>(p, s.D[1]); });
     tracked(cm, FD_K_PXX, st, [&] { d2_axis_kernel<R, 0, NDIM><<<grid, blk, 0, st>>>(p, s.D[0]); });
     tracked(cm, FD_K_TIME, st,
             [&] { time_update_kernel<R, NDIM><<<grid, blk, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });

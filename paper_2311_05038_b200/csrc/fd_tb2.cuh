@@ -59,10 +59,19 @@ __device__ __forceinline__ void role_release(B *...bars) {
 // halo loads they replace read 4 B at a 16 B lane stride -- 4-way bank
 // conflicts, 76 % of the excess shared wavefronts of the r05f profile.  Every
 // lane of the warp must execute this (full-mask shuffles).
-template <int R>
+// FD_XSHFL_3D: 0 (default) the halo quads from shared memory; 1 shuffles in
+// both stages of tb2ws, 2 stage B only, 3 stage A only.  r2 A/B on B200
+// (scripts/ab.sh, C3 order 2, 200-step runs): shared-memory halos 622.8 Gpts/s,
+// shuffles in both stages 599.5 -- the shuffles sit on the dependent chain
+// after the z-queue value and add the edge-lane branches; the 2D kernel lost
+// 4 % (C2 order 2) and 12 % (order 4) with them, so it keeps its loads.
+#ifndef FD_XSHFL_3D
+#define FD_XSHFL_3D 0
+#endif
+template <int R, bool SHFL>
 __device__ __forceinline__ void quad_xtaps(float (&av)[12], const float4 M4, const float *lq, bool needL, bool needR) {
     av[4] = M4.x; av[5] = M4.y; av[6] = M4.z; av[7] = M4.w;
-    if constexpr (R <= 2) {
+    if constexpr (SHFL && R <= 2) {
 #pragma unroll
         for (int m = 1; m <= R; ++m) {
             av[4 - m] = __shfl_up_sync(0xffffffffu, f4(M4, 4 - m), 1);
@@ -277,7 +286,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 for (int yy = 0; yy < C::NYA; ++yy) {
                     const int re = re0 + yy;
                     float av[12];
-                    quad_xtaps<R>(av, qz[(PH + R) % Q][yy], tc + (re + R) * C::BX0 + 4 * q, needL, needR);
+                    quad_xtaps<R, FD_XSHFL_3D == 1 || FD_XSHFL_3D == 3>(av, qz[(PH + R) % Q][yy], tc + (re + R) * C::BX0 + 4 * q, needL, needR);
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kza) : lds128(tk + offe);
                     const bool iny = (ymask >> yy) & 1u;
@@ -432,7 +441,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 const int re = ri0 + yy + R;
                 const int offe = re * C::BXE + 4 * q;
                 float av[12];
-                quad_xtaps<R>(av, qz[(PH + R) % Q][yy], t1c + offe - 4, needL, needR);
+                quad_xtaps<R, FD_XSHFL_3D == 1 || FD_XSHFL_3D == 2>(av, qz[(PH + R) % Q][yy], t1c + offe - 4, needL, needR);
                 const float4 pk4 = lds128(tpk + (re + R) * C::BX0 + 4 * q + 4);
                 const float4 k4 = KZ ? splat4(kzb) : lds128(tk + offe);
                 const bool iny = (ymask >> yy) & 1u;
@@ -608,7 +617,6 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
 #pragma unroll
         for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
-        const bool needL = lane == 0 || q == 0, needR = lane == 31 || q == C::QXE - 1;
         uint32_t smask = 0;
         for (int s2 = 0; s2 < prm.nsrc; ++s2)
             if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
@@ -624,15 +632,16 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             float4 oraw[C::NYA];                                   // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-            {   // all lanes (inactive ones compute on row 0 / quad 0 and store nothing): the x taps shuffle
+            if (act) {
                 float4 col[C::NYA + 2 * R];
 #pragma unroll
                 for (int i = 0; i < C::NYA + 2 * R; ++i) col[i] = lds128(tp + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
                     const int re = re0 + yy, z = rb - R + re;
-                    float av[12];
-                    quad_xtaps<R>(av, col[yy + R], tp + (re + R) * C::BX0 + 4 * q, needL, needR);
+                    const float *row = tp + (re + R) * C::BX0 + 4 * q;
+                    const float4 L4 = lds128(row), M4 = col[yy + R], R4 = lds128(row + 8);
+                    const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                     const int offe = re * C::BXE + 4 * q;
                     const float4 pm4 = lds128(tpm + offe), k4 = KZ ? splat4(kplane(prm, z)) : lds128(tk + offe);
                     const int gz = (int)prm.gz0 + z;
@@ -662,8 +671,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                             f4set(o, dx, __fadd_rn(f4(o, dx), wv[s2]));
                         }
                     }
-                    if (act) *reinterpret_cast<float4 *>(t1 + offe) = o;
-                    if (act && interior && xb < (int)prm.pitch) {
+                    *reinterpret_cast<float4 *>(t1 + offe) = o;
+                    if (interior && xb < (int)prm.pitch) {
                         *reinterpret_cast<float4 *>(prm.pnext + (int64_t)(z + halo_planes(R)) * prm.pitch + xb) = o;
                         if (anyp) peer_store4<R>(prm.peer1, z, (int)prm.nz, prm.pitch, xb, o);
                     }
@@ -688,7 +697,6 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const bool act = tb < C::NTB;
     const int qi = act ? tb % C::QXI : 0, ri0 = act ? (tb / C::QXI) * C::NYB : 0;
     const int q = qi + 1, xb = x0 + 4 * qi;
-    const bool needL = lane == 0 || qi == 0, needR = lane == 31 || qi == C::QXI - 1;
     bool inx[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
@@ -708,7 +716,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         const float *t1 = sP1 + s1 * C::EF;
         const int zt = rb + ri0;
         float4 out[C::NYB];
-        {   // all lanes (inactive ones compute on row 0 and store nothing): the x taps shuffle
+        if (act) {
             float4 col[C::NYB + 2 * R];
 #pragma unroll
             for (int i = 0; i < C::NYB + 2 * R; ++i) col[i] = lds128(t1 + (ri0 + i) * C::BXE + 4 * q);
@@ -716,8 +724,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             for (int yy = 0; yy < C::NYB; ++yy) {
                 const int re = ri0 + yy + R;
                 const int offe = re * C::BXE + 4 * q;
-                float av[12];
-                quad_xtaps<R>(av, col[yy + R], t1 + offe - 4, needL, needR);
+                const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
+                const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
                 const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4);
                 const float4 k4 = KZ ? splat4(kplane(prm, zt + yy)) : lds128(tk + offe);
                 const int gz = (int)prm.gz0 + zt + yy;

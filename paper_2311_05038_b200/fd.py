@@ -9,12 +9,15 @@ fallback: if libfd.so is missing, importing this module raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libfd.so"
+# FD_LIB: another in-tree build of the same library (A/B experiments,
+# scripts/ab.sh); the default is the package's libfd.so
+LIB_PATH = Path(os.environ["FD_LIB"]).resolve() if os.environ.get("FD_LIB") else _PKG / "libfd.so"
 
 FD_OK, FD_ERR_ARG, FD_ERR_RANGE, FD_ERR_UNSTABLE = 0, -1, -2, -3
 FD_ERR_NOMEM, FD_ERR_CUDA, FD_ERR_NCCL, FD_ERR_STATE = -4, -5, -6, -7
