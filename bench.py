@@ -409,6 +409,8 @@ def run_ours(args, wl):
     opts[fd.FD_OPT_TSTEPS] = args.tsteps
     if args.kplane:
         opts[fd.FD_OPT_KPLANE] = 1
+    if args.tb2tile >= 0:
+        opts[fd.FD_OPT_TB2TILE] = args.tb2tile
     sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport,
                     sponge=args.sponge)
     sim.step(args.warmup)
@@ -671,6 +673,8 @@ def main(argv=None):
                          "not the headline)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
+    ap.add_argument("--tb2tile", type=int, default=-1,
+                    help="FD_OPT_TB2TILE: pin a two-step kernel configuration (tuning; -1 = auto)")
     ap.add_argument("--reps", type=int, default=5,
                     help="repetitions of the K timed steps (value = the median repetition; min/median/max reported)")
     ap.add_argument("--launch-check", action="store_true",

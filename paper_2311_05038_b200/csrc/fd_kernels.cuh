@@ -1131,14 +1131,33 @@ __global__ void gather_receivers_kernel(const StepParams prm) {
 // K = fl32((v dt / h)^2 / scale) in fp64 (R#7), in place over the uploaded
 // velocities of a pitched buffer; explicit _rn intrinsics, so the result is
 // bitwise the host formula ((double)v * dt / h, squared, / scale, rounded once).
+// It also validates the model on the device (fd_create): the max velocity as
+// float bits (v > 0, so the bit patterns order like the values) for the CFL
+// check of R#8, and the smallest host index of an entry that is not finite and
+// > 0 (`bad`, initialised to ULLONG_MAX); idx0 = host index of buffer row 0.
 static __global__ void velocity_to_K_kernel(float *buf, int64_t rows, int64_t nx, int64_t pitch, double dt, double h,
-                                     double scale) {
+                                            double scale, int64_t idx0, unsigned *vmax_bits,
+                                            unsigned long long *bad) {
     const int64_t total = rows * nx;
+    unsigned m = 0;
+    unsigned long long b = ~0ull;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = (t / nx) * pitch + t % nx;
-        const double cv = __ddiv_rn(__dmul_rn((double)buf[i], dt), h);
+        const float v = buf[i];
+        if (v > 0.f && v <= 3.402823466e38f) m = max(m, __float_as_uint(v));
+        else b = min(b, (unsigned long long)(idx0 + t));
+        const double cv = __ddiv_rn(__dmul_rn((double)v, dt), h);
         buf[i] = __double2float_rn(__ddiv_rn(__dmul_rn(cv, cv), scale));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (m) atomicMax(vmax_bits, m);
+        if (b != ~0ull) atomicMin(bad, b);
     }
 }
 

@@ -371,7 +371,9 @@ static void destroy_all(fd_ctx *c) {
 // Allocate a slab's buffers and upload its K: from host velocities v (the
 // slab's planes; K halos zero until exchanged), or -- when v is NULL -- copied
 // with its r halo planes from a device K-halo buffer kdevh (planes z - r ..).
-static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kdevh = nullptr) {
+// Allocate a slab's buffers (fields zeroed); K is copied from kdevh (another
+// context's K halo buffer: virtual slabs) or zeroed for the caller's upload.
+static fd_status build_slab(fd_ctx *c, Slab &s, const float *kdevh) {
     const size_t fbytes = (size_t)buf_floats(c, s) * 4;
     const size_t kbytes = (size_t)((s.nz + 2 * c->R) * plane_floats(c)) * 4;
     s.F[0] = (float *)dev_alloc(fbytes);
@@ -382,31 +384,14 @@ static fd_status build_slab(fd_ctx *c, Slab &s, const float *v, const float *kde
     if (!s.F[0] || !s.F[1] || !s.Kh || !s.d_src_raw)
         return fail(FD_ERR_NOMEM, "device allocation of %.3f GB failed", (2.0 * fbytes + kbytes) / 1e9);
     c->dev_bytes += 2.0 * fbytes + kbytes;
-    if (v) {
-        CUDA_TRY(c, cudaMemset(s.Kh, 0, kbytes));
-        // upload v into the pitched K buffer, then K = fl32((v dt/h)^2/scale)
-        // in fp64 on the device (bitwise the host formula, R#7)
-        CUDA_TRY(c, cudaMemcpy2D(s.K, c->pitch * 4, v, c->nxg * 4, c->nxg * 4, c->nyg * s.nz,
-                                 cudaMemcpyHostToDevice));
-        const int64_t rows = c->nyg * s.nz;
-        const int blocks = (int)std::min<int64_t>((rows * c->nxg + 255) / 256, 148 * 32);
-        velocity_to_K_kernel<<<blocks, 256>>>(s.K, rows, c->nxg, c->pitch, c->dt, c->h, scale_of(c->R));
-        CUDA_TRY(c, cudaGetLastError());
-    } else if (kdevh) {
-        CUDA_TRY(c, cudaMemcpy(s.Kh, kdevh, kbytes, cudaMemcpyDeviceToDevice));
-    } else {
-        CUDA_TRY(c, cudaMemset(s.Kh, 0, kbytes));      // K uploaded by the caller (create_impl)
-    }
+    if (kdevh) CUDA_TRY(c, cudaMemcpy(s.Kh, kdevh, kbytes, cudaMemcpyDeviceToDevice));
+    else CUDA_TRY(c, cudaMemset(s.Kh, 0, kbytes));      // K uploaded by the caller (create_impl)
     CUDA_TRY(c, cudaMemset(s.F[0], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.F[1], 0, fbytes));
     CUDA_TRY(c, cudaMemset(s.d_src_raw, 0, kMaxSources * 4));
     return FD_OK;
 }
 
-// Host validation of velocities (R#7/R#8 inputs): returns the index of the
-// first entry that is not finite and > 0 (-1 if none) and the max.  Threaded;
-// blocks of 4096 with a branch-free (vectorisable) body, the failing entry
-// located only inside a failing block.
 static int64_t scan_velocity(const float *v, int64_t n, double *vmax_out) {
     int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
     nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, n / (1 << 20) + 1));
@@ -520,41 +505,40 @@ static fd_status create_impl(fd_ctx **out, int ndim, const int64_t *dims, double
     c->slabs.resize(1);
     Slab &s = c->slabs[0];
     s.z0 = z0; s.z1 = z1; s.nz = nz;
-    fd_status st = build_slab(c, s, nullptr, nullptr);
+    fd_status st = build_slab(c, s, nullptr);
     if (st == FD_OK) {
-        // Pipelined model upload (P:119 copy-in): validate a chunk of planes on
-        // the host (finite, > 0, running max for the CFL check of R#8) while the
-        // previous chunk's H2D copy and K conversion run on the device; an
-        // invalid model frees everything and reports as before.
-        cudaStream_t up = nullptr;
-        cudaError_t e = cudaStreamCreate(&up);   // blocking: ordered after build_slab's memsets
-        const int64_t pf = plane_floats(c);
-        const int64_t cz = std::max<int64_t>(1, ((int64_t)32 << 20) / std::max<int64_t>(1, plane * 4));
-        double vmax = 0;
-        int64_t bad = -1;
-        for (int64_t za = 0; za < nz && e == cudaSuccess; za += cz) {
-            const int64_t zb = std::min(nz, za + cz);
-            double vm = 0;
-            const int64_t b = scan_velocity(vloc + za * plane, (zb - za) * plane, &vm);
-            if (b >= 0) { bad = za * plane + b; break; }
-            vmax = std::max(vmax, vm);
-            e = cudaMemcpy2DAsync(s.K + za * pf, c->pitch * 4, vloc + za * plane, nxg * 4, nxg * 4, nyg * (zb - za),
-                                  cudaMemcpyHostToDevice, up);
-            if (e != cudaSuccess) break;
-            const int64_t rows = nyg * (zb - za);
+        // Model upload (P:119 copy-in): one H2D copy into the pitched K buffer,
+        // then one kernel converts v to K and validates the model on the device
+        // (finite and > 0, the max for the CFL check of R#8) -- a host scan of
+        // the model cost as much as the copy (C3: 512 MB); an invalid model
+        // frees everything and reports as the host check did.
+        unsigned *d_vmax = nullptr;
+        unsigned long long *d_bad = nullptr;
+        cudaError_t e = cudaMalloc(&d_vmax, 16);    // [0]: max bits, bytes 8..15: bad index
+        if (e == cudaSuccess) {
+            d_bad = reinterpret_cast<unsigned long long *>(d_vmax + 2);
+            e = cudaMemset(d_vmax, 0, sizeof(unsigned));
+        }
+        if (e == cudaSuccess) e = cudaMemset(d_bad, 0xff, sizeof(unsigned long long));
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(s.K, c->pitch * 4, vloc, nxg * 4, nxg * 4, nyg * nz, cudaMemcpyHostToDevice, 0);
+        if (e == cudaSuccess) {
+            const int64_t rows = nyg * nz;
             const int blocks = (int)std::min<int64_t>((rows * nxg + 255) / 256, 148 * 32);
-            velocity_to_K_kernel<<<blocks, 256, 0, up>>>(s.K + za * pf, rows, nxg, c->pitch, dt, h, scale_of(R));
+            velocity_to_K_kernel<<<blocks, 256>>>(s.K, rows, nxg, c->pitch, dt, h, scale_of(R), 0, d_vmax, d_bad);
             e = cudaGetLastError();
         }
-        if (up) {
-            const cudaError_t e2 = cudaStreamSynchronize(up);
-            if (e == cudaSuccess) e = e2;
-            cudaStreamDestroy(up);
-        }
+        unsigned vbits = 0;
+        unsigned long long bad = ~0ull;
+        if (e == cudaSuccess) e = cudaMemcpy(&vbits, d_vmax, sizeof vbits, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost);
+        if (d_vmax) cudaFree(d_vmax);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        float vmaxf;
+        memcpy(&vmaxf, &vbits, sizeof vmaxf);
         if (e != cudaSuccess) st = fail(FD_ERR_CUDA, "device setup failed: %s", cudaGetErrorString(e));
-        else if (bad >= 0) st = bad_fail(bad);
-        else st = cfl_fail(vmax);
+        else if (bad != ~0ull) st = bad_fail((int64_t)bad);
+        else st = cfl_fail((double)vmaxf);
     }
     if (st != FD_OK) {
         destroy_all(c);
@@ -763,7 +747,7 @@ static fd_status split_virtual(fd_ctx *c, int n) {
         int64_t a, b;
         partition(nz, n, q, &a, &b);
         s.z0 = c->z0 + a; s.z1 = c->z0 + b; s.nz = b - a;
-        st = build_slab(c, s, nullptr, o.Kh + a * pf);     // K planes a - r .. b + r
+        st = build_slab(c, s, o.Kh + a * pf);     // K planes a - r .. b + r
         if (st) break;
         const size_t bytes = (size_t)(s.nz * pf) * 4;
         for (int f = 0; f < 2; ++f)
@@ -1230,7 +1214,7 @@ static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStrea
                                 : dim3(gx, (unsigned)((s.nz + 7) / 8), 1u);
     const dim3 blk(32, 8);
     // fd_pzz / fd_pyy stream ZB points along their axis per thread
-    constexpr int ZB = 32;
+    constexpr int ZB = NDIM == 3 ? 32 : 16;      // 2D: more blocks for the short kernels
     const unsigned nzb = (unsigned)((s.nz + ZB - 1) / ZB);
     const dim3 gz = NDIM == 3 ? dim3(gx, (unsigned)((c->nyg + 7) / 8), nzb)
                               : dim3((unsigned)((c->nxg + 1023) / 1024), nzb, 1u);
