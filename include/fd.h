@@ -217,7 +217,7 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *                    2: temporal blocking -- one launch advances two steps (reads
  *                    p, p_prev, K once, writes both new fields: 10 B instead of
  *                    16 B per grid-point update); bitwise equal
- *                    to single steps.  2D any order, 3D order <= 4; on z-slabs
+ *                    to single steps.  2D and 3D, orders 2-8; on z-slabs
  *                    (ranks, FD_OPT_VSLABS) 2r + r halo planes per two steps.
  *   FD_OPT_TB2TILE   index of the temporal-blocking tile configuration (-1 auto)
  *   FD_OPT_RESERVE   n >= 0: finish setup now -- allocate the step tables for n more

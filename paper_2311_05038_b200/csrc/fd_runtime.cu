@@ -995,9 +995,8 @@ static fd_status prepare(fd_ctx *c) {
         }
     }
     if (c->opt_tsteps == 2) {
-        // temporal blocking: 3D r <= 2 or 2D, fused path
-        if ((c->ndim == 3 && c->R > 2) || c->opt_kernel != 0)
-            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs the fused kernel (3D: r <= 2)");
+        // temporal blocking (3D orders 2-8, 2D), fused path
+        if (c->opt_kernel != 0) return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs the fused kernel");
         const auto &tb = tb2_table();
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
             if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
@@ -2113,8 +2112,6 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         return FD_OK;
     case FD_OPT_TSTEPS:
         if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_TSTEPS must be 0 (auto), 1 or 2");
-        if (v == 2 && c->ndim == 3 && c->R > 2)
-            return fail(FD_ERR_ARG, "FD_OPT_TSTEPS=2 is implemented for 2D grids and 3D grids with order <= 4");
         c->opt_tsteps = (int)v;
         return FD_OK;
     case FD_OPT_TB2TILE:

@@ -6,9 +6,9 @@
 
 FD_LAUNCHER(launch_tb2d, tb2d_step_kernel)
 
-template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1, bool FULL = false, bool BG = false>
+template <int R, int TX, int TY, int NYA, int NYB, int NS, int N1, int MINB = 1, bool FULL = false>
 static TileCfg make_tb2d() {
-    using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB, BG>;
+    using C = CfgWS2<R, TX, TY, NYA, NYB, NS, N1, MINB>;
     TileCfg t{2, R, TX, TY, NYB, NS, N1, C::BX0, C::BXE, C::BY0, C::BYE, C::NTHREADS, C::SMEM_BYTES, {}, {}};
     FD_VARIANTS(t, C, FULL, tb2d_step_kernel, launch_tb2d);
     return t;
@@ -28,8 +28,8 @@ std::vector<TileCfg> fdtab::tb2d() {
         make_tb2d<3, 64, 26, 4, 2, 3, 2, 1, true>(), make_tb2d<3, 64, 26, 2, 2, 3, 2>(),
         make_tb2d<4, 64, 24, 4, 4, 3, 2, 1, true>(), make_tb2d<4, 64, 24, 4, 3, 3, 2>(),
         make_tb2d<1, 128, 30, 2, 3, 3, 2, 1>(),
-        // r2: stage B's P^k / K rows from global (BG; stages released by A alone)
-        make_tb2d<1, 64, 30, 2, 3, 3, 2, 2, false, true>(), make_tb2d<1, 64, 30, 2, 3, 2, 2, 2, false, true>(),
-        make_tb2d<2, 64, 40, 4, 4, 2, 2, 2, false, true>(), make_tb2d<2, 64, 28, 4, 4, 3, 2, 1, false, true>(),
-        make_tb2d<2, 64, 40, 4, 4, 3, 2, 1, false, true>()};
+        // r2: 56-column tiles (4096 = 73.1 columns of 56: 74 x 4 chunks = 296
+        // CTAs = one wave of two CTAs per SM on C2, vs 64 x 9 = 576 = 1.95 waves)
+        make_tb2d<1, 56, 30, 2, 3, 3, 2, 2>(), make_tb2d<1, 56, 30, 2, 2, 3, 2, 2>(),
+        make_tb2d<2, 56, 40, 4, 4, 2, 2, 2>(), make_tb2d<2, 56, 40, 4, 2, 2, 2, 2>()};
 }

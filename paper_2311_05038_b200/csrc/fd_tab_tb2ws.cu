@@ -1,4 +1,4 @@
-// fd_tab_tb2ws.cu -- two-steps-per-pass (temporal blocking) tiles, 3D, r <= 2
+// fd_tab_tb2ws.cu -- two-steps-per-pass (temporal blocking) tiles, 3D
 // (fd_tb2.cuh; see fd_tables.cuh).  Presented as TileCfg so the chunking /
 // receiver code is shared: pbw/pbz hold the P^k box (BX0, BY0), tbw/tbz the
 // grown-tile box (BXE, BYE).
@@ -34,5 +34,9 @@ std::vector<TileCfg> fdtab::tb2ws() {
         // r05 role-balance sweep (3D r=1, 128 x 16): stage-A rows per thread
         // NYA / stage-B rows NYB -> warps 7+4, 10+8, 7+8, 4+4
         make_tb2ws<1, 128, 16, 3, 4, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 2, 2, 3, 3, 2, 1>(),
-        make_tb2ws<1, 128, 16, 3, 2, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 6, 4, 3, 3, 2, 1>()};
+        make_tb2ws<1, 128, 16, 3, 2, 3, 3, 2, 1>(), make_tb2ws<1, 128, 16, 6, 4, 3, 3, 2, 1>(),
+        // r2: 3D r = 3, 4 (orders 6, 8), tuning-only (FD_OPT_TSTEPS=2): 64 x 16
+        // tiles, stage A on the 72 x (16 + 2r) grown tile (1.6-1.7x the points)
+        make_tb2ws<3, 64, 16, 2, 2, 1, 1, 1>(), make_tb2ws<4, 64, 16, 2, 2, 0, 0, 0>(),
+        make_tb2ws<4, 64, 16, 1, 2, 0, 0, 0>()};
 }

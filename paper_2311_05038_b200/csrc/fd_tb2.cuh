@@ -534,15 +534,9 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
 // compute P^{k+2} on the block from it (to D), one block behind.  Blocks are
 // self-contained (their z halo rows come with the box), so the P1 ring only
 // decouples A from B.  20 B per point per launch = 10 B per update.
-// BG: stage B reads its pointwise P^k and K rows from global memory (L2: the
-// producer's TMA brought them in microseconds earlier) instead of the stage,
-// so a stage is released by stage A alone and the producer runs up to NS - 1
-// blocks ahead of A (with B one block behind A, a 2-stage ring otherwise
-// leaves no stage free to prefetch into).
-template <int R_, int TX_, int TY_, int NYA_, int NYB_, int NS_, int N1_, int MINB_ = 1, bool BG_ = false>
+template <int R_, int TX_, int TY_, int NYA_, int NYB_, int NS_, int N1_, int MINB_ = 1>
 struct CfgWS2 {
     static constexpr int R = R_, TX = TX_, TY = TY_, NYA = NYA_, NYB = NYB_, NS = NS_, N1 = N1_, MINB = MINB_;
-    static constexpr bool BG = BG_;
     static constexpr int BX0 = TX + 16, BY0 = TY + 4 * R;         // P^k block (x halo 8, z halo 2r)
     static constexpr int BXE = TX + 8, BYE = TY + 2 * R;          // grown block E
     static constexpr int QXE = BXE / 4, QXI = TX / 4;
@@ -581,10 +575,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
     const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
     if (tid == 0) {
-        for (int i = 0; i < C::NS; ++i) {
-            mbar_init(&fullS[i], 1);
-            mbar_init(&emptyS[i], kArrivalsPerWarp * (C::BG ? C::NWA : C::NWA + C::NWB));
-        }
+        for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], kArrivalsPerWarp * (C::NWA + C::NWB)); }
         for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], kArrivalsPerWarp * C::NWA); mbar_init(&empty1[i], kArrivalsPerWarp * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -725,17 +716,6 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         const float *t1 = sP1 + s1 * C::EF;
         const int zt = rb + ri0;
         float4 out[C::NYB];
-        float4 gpk[C::NYB], gk[C::NYB];                // BG: this thread's P^k / K rows from global
-        if constexpr (C::BG) {
-#pragma unroll
-            for (int yy = 0; yy < C::NYB; ++yy) {
-                const bool in = act && zt + yy < prm.zhi && xb < (int)prm.pitch;
-                gpk[yy] = in ? __ldg(reinterpret_cast<const float4 *>(prm.p + (int64_t)(zt + yy + halo_planes(R)) * prm.pitch + xb))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                gk[yy] = (in && !KZ) ? __ldg(reinterpret_cast<const float4 *>(prm.K + (int64_t)(zt + yy) * prm.pitch + xb))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
         if (act) {
             float4 col[C::NYB + 2 * R];
 #pragma unroll
@@ -746,8 +726,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 const int offe = re * C::BXE + 4 * q;
                 const float4 L4 = lds128(t1 + offe - 4), M4 = col[yy + R], R4 = lds128(t1 + offe + 4);
                 const float av[12] = {L4.x, L4.y, L4.z, L4.w, M4.x, M4.y, M4.z, M4.w, R4.x, R4.y, R4.z, R4.w};
-                const float4 pk4 = C::BG ? gpk[yy] : lds128(tp + (re + R) * C::BX0 + 4 * q + 4);
-                const float4 k4 = KZ ? splat4(kplane(prm, zt + yy)) : (C::BG ? gk[yy] : lds128(tk + offe));
+                const float4 pk4 = lds128(tp + (re + R) * C::BX0 + 4 * q + 4);
+                const float4 k4 = KZ ? splat4(kplane(prm, zt + yy)) : lds128(tk + offe);
                 const int gz = (int)prm.gz0 + zt + yy;
                 const bool inz = (gz >= R) && (gz < (int)prm.nzg - R);
                 const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
@@ -767,8 +747,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 }
             }
         }
-        if constexpr (C::BG) role_release(&empty1[s1]);
-        else role_release(&empty1[s1], &emptyS[s]);
+        role_release(&empty1[s1], &emptyS[s]);
         if (rp < rend && prm.rec.z[rp] < rb + C::TY)                  // owners: B threads
             rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
                                      [&](int i, int &ln, int &yy, int &e) {

@@ -400,7 +400,7 @@ def test_cuda_graph_replay_bitwise(fd, dims, kernel):
 # Temporal blocking (FD_OPT_TSTEPS=2): two steps per launch, bitwise = single
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dims,order", [((37, 45, 70), 2), ((30, 33, 131), 2), ((41, 29, 66), 4),
-                                        ((24, 70, 140), 4)])
+                                        ((24, 70, 140), 4), ((33, 40, 70), 6), ((35, 36, 130), 8)])
 def test_temporal_blocking_bitwise(fd, oracle, dims, order):
     from paper_2311_05038_b200 import fd as fdm
     vel = _rand_vel(dims, seed=37)
@@ -412,7 +412,7 @@ def test_temporal_blocking_bitwise(fd, oracle, dims, order):
     recs = [tuple(d // 2 for d in dims), (dims[0] // 3, 15, 63), (dims[0] - 3, 17, 5), (1, 1, 1)]
     ref = run_gpu(fd, vel, h, dt, order, 41, src, recs)
     ntb = 0
-    for tile in range(16):
+    for tile in range(64):
         for zc in (0, 1, 3):
             for graph in (1, 0):
                 try:
@@ -464,7 +464,8 @@ def test_reserve_then_step_bitwise(fd):
             assert np.array_equal(a, b), ts
 
 
-@pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((41, 29, 66), 4), ((96, 300), 2), ((70, 140), 8)])
+@pytest.mark.parametrize("dims,order", [((40, 30, 70), 2), ((41, 29, 66), 4), ((60, 29, 66), 8), ((96, 300), 2),
+                                        ((70, 140), 8)])
 @pytest.mark.parametrize("nslabs", [2, 3, 7])
 def test_temporal_blocking_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs):
     """Two steps per launch on z-slabs (2r halo planes of P^{k+2}, r of
@@ -517,7 +518,7 @@ def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     recs = [(dims[0] // 2, dims[1] // 2), (29, 63), (dims[0] - 3, 5), (1, 1), (60, 130 % dims[1])]
     ref = run_gpu(fd, vel, h, dt, order, 41, src, recs, options={fd.FD_OPT_TSTEPS: 1})
     ntb = 0
-    for tile in range(32):
+    for tile in range(64):
         for zc in (0, 1, 3):
             for graph in (1, 0):
                 try:
