@@ -411,6 +411,8 @@ def run_ours(args, wl):
         opts[fd.FD_OPT_KPLANE] = 1
     if args.tb2tile >= 0:
         opts[fd.FD_OPT_TB2TILE] = args.tb2tile
+    if args.zchunks > 0:
+        opts[fd.FD_OPT_ZCHUNKS] = args.zchunks
     sim = _make_sim(wl, world, vel, gdims, stream=stream.cuda_stream, options=opts, transport=args.transport,
                     sponge=args.sponge)
     sim.step(args.warmup)
@@ -444,7 +446,7 @@ def run_ours(args, wl):
             if world > 1:
                 torch.distributed.barrier()
             rep_ms.append(ev0.elapsed_time(ev1))
-    launches = (sim.info()["kernel_launches"] - launches0) / args.reps
+    launches = int(round((sim.info()["kernel_launches"] - launches0) / args.reps))   # per timed repetition
     if world > 1:
         t = torch.tensor(rep_ms, dtype=torch.float64,
                          device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
@@ -675,6 +677,8 @@ def main(argv=None):
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     ap.add_argument("--tb2tile", type=int, default=-1,
                     help="FD_OPT_TB2TILE: pin a two-step kernel configuration (tuning; -1 = auto)")
+    ap.add_argument("--zchunks", type=int, default=0,
+                    help="FD_OPT_ZCHUNKS: pin the z-chunk count (tuning; 0 = auto)")
     ap.add_argument("--reps", type=int, default=5,
                     help="repetitions of the K timed steps (value = the median repetition; min/median/max reported)")
     ap.add_argument("--launch-check", action="store_true",

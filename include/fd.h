@@ -66,6 +66,9 @@ enum { FD_FLAG_ALLOW_UNSTABLE = 1u /* skip the CFL refusal (S:553 --allow-unstab
  *   vel    host, prod(dims) fp32 velocities, all finite and > 0; copied.
  *          Stored on the device as K = (v dt / h)^2 / scale (computed in fp64,
  *          rounded once), the only per-point coefficient of the update (R#7).
+ *          Validated on the device after the one copy (the K conversion
+ *          kernel checks each entry and reduces max(v) for the CFL check);
+ *          pinned host memory makes the copy asynchronous DMA.
  *   flags  FD_FLAG_ALLOW_UNSTABLE to skip the CFL check (R#8).
  * Initial state: P^0 = P^-1 = 0 (R#12), no sources, no receivers, k = 0.
  * Errors: FD_ERR_ARG, FD_ERR_UNSTABLE, FD_ERR_NOMEM, FD_ERR_CUDA.  On error *out = NULL. */

@@ -102,6 +102,7 @@ struct StepParams {
     int32_t zlo, zhi;       // local planes computed by this launch
     int32_t ntx, nty;       // tiles along x, y
     int32_t nchunks;        // z-chunks of [zlo, zhi)
+    int32_t lin;            // tb2d linear mode: units sharing the ntx * nb blocks (0: chunked)
     float *pnext;           // base of the p_prev buffer (overwritten in place); TB2: the C buffer
     float *pnext2;          // TB2 only: the D buffer (P^{k+2})
     const float *p;         // base of the p buffer (naive kernel only)
@@ -384,13 +385,17 @@ __device__ __forceinline__ float4 stencil_row4(const float (&a)[12], YN yn, ZN z
 // by shuffle.  Every lane must call (warp-uniform); returns the index past the
 // run.  Replaces a per-thread serial scan whose dependent loads cost ~10 us on
 // a 256-receiver row.
+// `recx` (optional): also require x in [xlo, xhi) -- a unit that crosses
+// columns (tb2d linear mode) holds the next column's receivers of the same
+// rows right after this block's.
 template <int NY, class Owner>
 __device__ __forceinline__ int warp_record(const float4 (&out)[NY], const int32_t *recz, const int32_t *recid,
-                                           int rp, int rend, int zlo, int zhi, float *trace_row, Owner owner) {
+                                           int rp, int rend, int zlo, int zhi, float *trace_row, Owner owner,
+                                           const int32_t *recx = nullptr, int xlo = 0, int xhi = 0) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         const int i = rp + lane;
-        const bool valid = i < rend && recz[i] >= zlo && recz[i] < zhi;
+        const bool valid = i < rend && recz[i] >= zlo && recz[i] < zhi && (!recx || (recx[i] >= xlo && recx[i] < xhi));
         const unsigned m = __ballot_sync(0xffffffffu, valid);
         if (!m) break;
         int src = lane, yy = 0, e = 0;

@@ -185,6 +185,7 @@ struct RecDef {
 struct Region {
     int32_t zlo = 0, zhi = 0;
     int zchunks = 1;
+    int lin = 0;                // tb2d linear mode: units (one wave) sharing the region's blocks; 0: chunked
     int ctas = 0;
     bool boundary = false;      // launched on the comm stream before the exchange
     int32_t *d_rec = nullptr;   // [4 * nrec + units + 1]: z, y, x, id, CSR offsets
@@ -618,6 +619,19 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     return (int)best;
 }
 
+// 2D two-step launches (tb2d) split the region's ntx * nb row blocks into
+// one wave of equal contiguous ranges ("linear" units that cross column
+// boundaries): one pipeline warm-up per CTA and no wave tail, vs the chunked
+// split's whole columns x z-chunks (C2: 64 columns; 296 slots).
+// FD_OPT_ZCHUNKS pins the chunked split (FD_TB2D_LINEAR=0 too: A/B).
+static int lin_units(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
+    const bool tb2d = c->ndim == 2 && c->tb2 >= 0 && &t == &tb2_table()[c->tb2];
+    static const bool off = [] { const char *e = getenv("FD_TB2D_LINEAR"); return e && e[0] == '0'; }();
+    if (!tb2d || c->opt_zchunks > 0 || off) return 0;
+    const int64_t nb = (span + t.ty - 1) / t.ty, V = ((c->nxg + t.tx - 1) / t.tx) * nb;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)c->nsm * std::max(occ, 1)));
+}
+
 // Preferred tile per (ndim, r), from the r01 sweep: 3D r=1 128x16 (428 Gpts/s
 // on C3), r=2 128x32 (410), r>=3 64x16 with 2 rows/thread (379 at r=4); 2D
 // 64x32 blocks with 3 ring slots (363 / 347 on C2).  Falls back to the first
@@ -682,7 +696,7 @@ static fd_status make_maps(fd_ctx *c, Slab &s) {
 static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g, const TileCfg *t) {
     dev_free(g.d_rec);
     g.d_rec = nullptr;
-    struct L { int32_t unit, z, y, x, id; };
+    struct L { int32_t unit, z, y, x, id, key; };
     std::vector<L> loc;
     int ntx = 1, ntiles = 1;
     if (t) {
@@ -693,8 +707,15 @@ static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g, co
     for (size_t j = 0; j < c->rec.size(); ++j) {
         const int64_t lz = c->rec[j].g[0] - s.z0;
         if (lz < g.zlo || lz >= g.zhi) continue;
-        L l{0, (int32_t)lz, (int32_t)c->rec[j].g[1], (int32_t)c->rec[j].g[2], (int32_t)j};
-        if (t) {
+        L l{0, (int32_t)lz, (int32_t)c->rec[j].g[1], (int32_t)c->rec[j].g[2], (int32_t)j, 0};
+        if (t && g.lin > 0) {
+            // linear units (tb2d): block v = column * nb + row block, unit u
+            // holds [V u / G, V (u+1) / G); sorted by (unit, v, z)
+            const int64_t nb = (span + t->ty - 1) / t->ty, V = (int64_t)ntx * nb;
+            const int64_t v = (l.x / t->tx) * nb + (lz - g.zlo) / t->ty;
+            l.unit = (int32_t)(((v + 1) * g.lin - 1) / V);
+            l.key = (int32_t)v;
+        } else if (t) {
             // the chunk containing plane lz, as the kernels split [zlo, zhi):
             // 3D by planes, 2D by whole blocks of ty rows
             int ch = 0;
@@ -709,9 +730,9 @@ static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g, co
         loc.push_back(l);
     }
     std::stable_sort(loc.begin(), loc.end(), [](const L &a, const L &b) {
-        return a.unit != b.unit ? a.unit < b.unit : a.z < b.z;
+        return a.unit != b.unit ? a.unit < b.unit : (a.key != b.key ? a.key < b.key : a.z < b.z);
     });
-    const int nunits = t ? ntiles * g.zchunks : 0;
+    const int nunits = t ? (g.lin > 0 ? g.lin : ntiles * g.zchunks) : 0;
     const int n = (int)loc.size();
     g.nrec = n;
     std::vector<int32_t> h((size_t)4 * n + nunits + 1, 0);
@@ -856,6 +877,7 @@ static void split_regions(const fd_ctx *c, const Slab &s, bool overlap, int32_t 
         Region g;
         g.zlo = lo; g.zhi = hi; g.boundary = boundary;
         g.zchunks = t ? chunks_for(c, *t, occ, hi - lo) : 1;
+        g.lin = t ? lin_units(c, *t, occ, hi - lo) : 0;
         out.push_back(g);
     };
     if (!overlap) { add(0, nz, false); return; }
@@ -1122,6 +1144,7 @@ static void fill_params(const fd_ctx *c, const Slab &s, const Region *g, StepPar
     p.zlo = g ? g->zlo : 0;
     p.zhi = g ? g->zhi : (int32_t)s.nz;
     p.nchunks = g ? g->zchunks : 1;
+    p.lin = g ? g->lin : 0;
     p.nsrc = (int32_t)c->src.size();
     for (int q = 0; q < p.nsrc; ++q) {
         p.sz[q] = (int32_t)(c->src[q].g[0] - s.z0);
@@ -1511,7 +1534,7 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     p.K = s.K;
     p.ntx = (int32_t)((c->nxg + t.tx - 1) / t.tx);
     p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
-    const dim3 grid((unsigned)(p.ntx * p.nty * p.nchunks));
+    const dim3 grid((unsigned)(p.lin > 0 ? p.lin : p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
     const bool push = c->opt_transport == 1 && g.boundary;
@@ -2199,7 +2222,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
         o->threads_per_cta = t.threads; o->smem_bytes = t.smem;
         int ctas = 0, zc = 0;
         for (auto &sl : c->slabs)
-            for (auto &g : sl.tb2) { ctas += (int)(ntiles_of(c, t) * g.zchunks); zc = std::max(zc, g.zchunks); }
+            for (auto &g : sl.tb2) { ctas += g.lin > 0 ? g.lin : (int)(ntiles_of(c, t) * g.zchunks); zc = std::max(zc, g.zchunks); }
         o->zchunks = zc;
         o->ctas = ctas;
         return FD_OK;

@@ -567,21 +567,35 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     uint64_t *fullS = bars, *emptyS = fullS + C::NS, *full1 = emptyS + C::NS, *empty1 = full1 + C::N1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool anyp = PEER;                          // in-kernel halo pushes (boundary launches)
+    // Work: blocks v = column * nb + block row, taken in order.  Chunked mode
+    // (prm.lin == 0): unit = chunk * ntx + column, a z-range of one column.
+    // Linear mode (prm.lin = G units, one wave): unit u takes the contiguous
+    // range [V u / G, V (u+1) / G) of the V = ntx * nb blocks, crossing column
+    // boundaries -- balanced to one block, one pipeline warm-up per CTA (blocks
+    // are self-contained: their z halo rows come with the box).
     const int unit = blockIdx.x;
-    const int chunk = unit / prm.ntx;
-    const int x0 = (unit - chunk * prm.ntx) * C::TX;
     const int span = prm.zhi - prm.zlo;
     const int nb = (span + C::TY - 1) / C::TY;
-    const int b0 = (int)(((int64_t)nb * chunk) / prm.nchunks);
-    const int b1 = (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
+    int v0, v1;
+    if (prm.lin > 0) {
+        const int64_t V = (int64_t)prm.ntx * nb;
+        v0 = (int)(V * unit / prm.lin);
+        v1 = (int)(V * (unit + 1) / prm.lin);
+    } else {
+        const int chunk = unit / prm.ntx, colu = unit - chunk * prm.ntx;
+        v0 = colu * nb + (int)(((int64_t)nb * chunk) / prm.nchunks);
+        v1 = colu * nb + (int)(((int64_t)nb * (chunk + 1)) / prm.nchunks);
+    }
     if (tid == 0) {
         for (int i = 0; i < C::NS; ++i) { mbar_init(&fullS[i], 1); mbar_init(&emptyS[i], kArrivalsPerWarp * (C::NWA + C::NWB)); }
         for (int i = 0; i < C::N1; ++i) { mbar_init(&full1[i], kArrivalsPerWarp * C::NWA); mbar_init(&empty1[i], kArrivalsPerWarp * C::NWB); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (b1 <= b0) return;
-    const int nload = b1 - b0;
+    if (v1 <= v0) return;
+    const int nload = v1 - v0;
+    // receiver i belongs to block v (receivers are sorted by (unit, v, z))
+    auto rec_block = [&](int i) { return (prm.rec.x[i] / C::TX) * nb + (prm.rec.z[i] - prm.zlo) / C::TY; };
     const int nx = (int)prm.nx;
     const int64_t kk = step_index(prm);
     constexpr float c0 = tap(R, 0);
@@ -592,7 +606,8 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         if (lane == 0) {
             tma_prefetch_desc(&map_p0); tma_prefetch_desc(&map_pm); tma_prefetch_desc(&map_k);
             for (int l = 0; l < nload; ++l) {
-                const int s = l % C::NS, rb = prm.zlo + (b0 + l) * C::TY;
+                const int v = v0 + l, colu = v / nb;
+                const int s = l % C::NS, rb = prm.zlo + (v - colu * nb) * C::TY, x0 = colu * C::TX;
                 mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
                 mbar_expect_tx(&fullS[s], C::STAGE_BYTES - (KZ ? C::BXE * C::BYE * 4 : 0));
                 float *st = sSt + s * C::STAGE;
@@ -609,22 +624,30 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         // ---------------------------------------------------------------- stage A
         const bool act = tid < C::NTA;
         const int q = act ? tid % C::QXE : 0, re0 = act ? (tid / C::QXE) * C::NYA : 0;
-        const int xb = x0 - 4 + 4 * q;
-        bool inx[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
-        float sgx[4];                                  // sponge factors (SP only)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
         const bool qint = q >= 1 && q <= C::QXI;
+        // per-column state (recomputed when the block moves to another column)
+        int colc = -1, x0 = 0, xb = 0;
+        bool inx[4];
+        float sgx[4];                                  // sponge factors (SP only)
         uint32_t smask = 0;
-        for (int s2 = 0; s2 < prm.nsrc; ++s2)
-            if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
         float *const trow = trace_row_of(prm, kk);
         const float *const wv = w_next_of(prm, kk);
         for (int l = 0; l < nload; ++l) {
             const int s = l % C::NS, s1 = l % C::N1;
-            const int rb = prm.zlo + (b0 + l) * C::TY;
+            const int v = v0 + l, colu = v / nb;
+            const int rb = prm.zlo + (v - colu * nb) * C::TY;
+            if (colu != colc) {
+                colc = colu;
+                x0 = colu * C::TX;
+                xb = x0 - 4 + 4 * q;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
+                smask = 0;
+                for (int s2 = 0; s2 < prm.nsrc; ++s2)
+                    if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
+            }
             mbar_wait(&fullS[s], (l / C::NS) & 1);
             mbar_wait(&empty1[s1], ((l / C::N1) & 1) ^ 1);
             const float *tp = sSt + s * C::STAGE, *tpm = tp + C::P0F, *tk = tpm + C::EF;
@@ -678,7 +701,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     }
                 }
             }
-            if (rp < rend && prm.rec.z[rp] < rb + C::TY)              // owners: block-interior A threads
+            if (rp < rend && rec_block(rp) == v)                      // owners: block-interior A threads
                 rp = warp_record<C::NYA>(oraw, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
                                          [&](int i, int &ln, int &yy, int &e) {
                                              const int re = prm.rec.z[i] - (rb - R), dx = prm.rec.x[i] - (x0 - 4);
@@ -686,7 +709,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                                              if ((t >> 5) != warp) return false;
                                              ln = t & 31; yy = re % C::NYA; e = dx & 3;
                                              return true;
-                                         });
+                                         }, prm.rec.x, x0, x0 + C::TX);
             role_release(&full1[s1], &emptyS[s]);
         }
         return;
@@ -696,21 +719,29 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
     const int tb = tid - 32 * C::NWA;
     const bool act = tb < C::NTB;
     const int qi = act ? tb % C::QXI : 0, ri0 = act ? (tb / C::QXI) * C::NYB : 0;
-    const int q = qi + 1, xb = x0 + 4 * qi;
+    const int q = qi + 1;
+    int colc = -1, x0 = 0, xb = 0;                     // per-column state
     bool inx[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
     float sgx[4];                                      // sponge factors (SP only)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
     uint32_t smask = 0;
-    for (int s2 = 0; s2 < prm.nsrc; ++s2)
-        if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
     float *const trow = trace_row_of(prm, kk + 1);
     const float *const wv = w_next_of(prm, kk + 1);
     for (int l = 0; l < nload; ++l) {
         const int s = l % C::NS, s1 = l % C::N1;
-        const int rb = prm.zlo + (b0 + l) * C::TY;
+        const int v = v0 + l, colu = v / nb;
+        const int rb = prm.zlo + (v - colu * nb) * C::TY;
+        if (colu != colc) {
+            colc = colu;
+            x0 = colu * C::TX;
+            xb = x0 + 4 * qi;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) inx[e] = (xb + e >= R) && (xb + e < nx - R);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sgx[e] = SP ? sponge_gx(prm, xb + e) : 1.f;
+            smask = 0;
+            for (int s2 = 0; s2 < prm.nsrc; ++s2)
+                if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
+        }
         mbar_wait(&full1[s1], (l / C::N1) & 1);
         const float *tp = sSt + s * C::STAGE, *tk = tp + C::P0F + C::EF;
         const float *t1 = sP1 + s1 * C::EF;
@@ -748,7 +779,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             }
         }
         role_release(&empty1[s1], &emptyS[s]);
-        if (rp < rend && prm.rec.z[rp] < rb + C::TY)                  // owners: B threads
+        if (rp < rend && rec_block(rp) == v)                          // owners: B threads
             rp = warp_record<C::NYB>(out, prm.rec.z, prm.rec.id, rp, rend, rb, rb + C::TY, trow,
                                      [&](int i, int &ln, int &yy, int &e) {
                                          const int dz = prm.rec.z[i] - rb, dx = prm.rec.x[i] - x0;
@@ -756,7 +787,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                                          if (C::NWA + (t >> 5) != warp) return false;
                                          ln = t & 31; yy = dz % C::NYB; e = dx & 3;
                                          return true;
-                                     });
+                                     }, prm.rec.x, x0, x0 + C::TX);
         if (!act) continue;
         if (smask) {
             for (int s2 = 0; s2 < prm.nsrc; ++s2) {

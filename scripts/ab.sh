@@ -14,10 +14,14 @@ IFS=';' read -ra CS <<< "${CASES}"
 for r in $(seq 1 $ROUNDS); do
   for c in "${CS[@]}"; do
     for v in ${VARIANTS}; do
+      # a variant is a library name (libfd_NAME.so; "default" = libfd.so) or
+      # env:VAR=VALUE (the default library with that environment variable)
       lib=paper_2311_05038_b200/libfd_${v}.so
+      envs=""
       [ "$v" = "default" ] && lib=paper_2311_05038_b200/libfd.so
+      case "$v" in env:*) lib=paper_2311_05038_b200/libfd.so; envs="${v#env:}";; esac
       echo "# $v | $c" >> $out
-      FD_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --no-e2e --sustained 0 --reps 5 $c >> $out 2>&1
+      env $envs FD_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --no-e2e --sustained 0 --reps 5 $c >> $out 2>&1
     done
   done
 done

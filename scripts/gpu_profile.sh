@@ -16,12 +16,12 @@ for spec in $SPECS; do
   # launch list (cold-cache, serialised): compare the step kernel's SHARE of the step
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
       --log-file gpurun_out/launches_${TAG}_${cfg}_o${ord}${sfx}.csv \
-      python bench.py --config $cfg --order $ord --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --tsteps $ts $kzf \
+      python bench.py --config $cfg --order $ord --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --reps 1 --tsteps $ts $kzf \
       > /dev/null 2>&1
   # full capture of one steady-state launch of the step kernel
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5 -c 1 \
       -o gpurun_out/prof_${TAG}_${cfg}_o${ord}${sfx} -f \
-      python bench.py --config $cfg --order $ord --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --tsteps $ts $kzf \
+      python bench.py --config $cfg --order $ord --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --reps 1 --tsteps $ts $kzf \
       > /dev/null 2>&1
 done
 ls -la gpurun_out

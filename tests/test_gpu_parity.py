@@ -536,6 +536,28 @@ def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
 
 
+@pytest.mark.parametrize("dims,order", [((600, 1100), 2), ((517, 1000), 4), ((430, 900), 8)])
+def test_tb2d_linear_units_cross_columns(fd, oracle, dims, order):
+    """2D two-step launches split the row blocks into one wave of contiguous
+    ranges that cross column boundaries (linear units): bitwise equal to the
+    chunked split (FD_OPT_ZCHUNKS pinned) and to single steps, with receivers
+    on a whole row and a whole column (several units' blocks, column
+    crossings) and sources on column / block faces."""
+    vel = _rand_vel(dims, seed=83)
+    h, dt = 10.0, 0.5e-3
+    nz, nx = dims
+    src = [((nz // 2, 64), 25.0, 0.02, 1.0), ((30, 127), 18.0, 0.03, -0.6), ((nz - 40, nx // 2), 12.0, 0.04, 0.5)]
+    recs = [(nz // 2 + 1, x) for x in range(0, nx, 3)] + [(z, 128) for z in range(0, nz, 2)] + [(29, 63), (30, 64)]
+    ref = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 1})
+    lin = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 2})
+    chk = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3})
+    assert lin[3]["steps_per_launch"] == 2
+    for a, b, c in zip(lin[:3], chk[:3], ref[:3]):
+        assert np.array_equal(a, c) and np.array_equal(b, c)
+    Po, _, To = oracle.run(vel, h, dt, order, 37, src, recs, nthreads=4)
+    assert rel_l2(lin[0], Po) <= TOL and rel_l2(lin[2], To) <= TOL
+
+
 # ---------------------------------------------------------------------------
 # Cluster-resident runs (FD_OPT_RESIDENT): one launch per fd_step call, the
 # fields in the cluster's shared memory, halos pushed through DSMEM
