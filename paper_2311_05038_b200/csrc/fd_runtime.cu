@@ -619,15 +619,19 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     return (int)best;
 }
 
-// 2D two-step launches (tb2d) split the region's ntx * nb row blocks into
+// 2D two-step launches (tb2d) can split the region's ntx * nb row blocks into
 // one wave of equal contiguous ranges ("linear" units that cross column
 // boundaries): one pipeline warm-up per CTA and no wave tail, vs the chunked
-// split's whole columns x z-chunks (C2: 64 columns; 296 slots).
-// FD_OPT_ZCHUNKS pins the chunked split (FD_TB2D_LINEAR=0 too: A/B).
+// split's whole columns x z-chunks.  Opt-in (FD_TB2D_LINEAR=1): r2 A/B on C2
+// (Gpts/s, linear vs chunked) 64-column tiles 331 vs 556 (order 2) and 319
+// vs 501 (order 4) -- the co-running CTAs sit ~900 rows apart in the same
+// columns instead of side by side in one z band, and lose the L2 sharing of
+// the x halos; 56-column tiles 547 vs 535 and 512 vs 490.  FD_OPT_ZCHUNKS
+// pins the chunked split.
 static int lin_units(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
     const bool tb2d = c->ndim == 2 && c->tb2 >= 0 && &t == &tb2_table()[c->tb2];
-    static const bool off = [] { const char *e = getenv("FD_TB2D_LINEAR"); return e && e[0] == '0'; }();
-    if (!tb2d || c->opt_zchunks > 0 || off) return 0;
+    static const bool on = [] { const char *e = getenv("FD_TB2D_LINEAR"); return e && e[0] == '1'; }();
+    if (!tb2d || c->opt_zchunks > 0 || !on) return 0;
     const int64_t nb = (span + t.ty - 1) / t.ty, V = ((c->nxg + t.tx - 1) / t.tx) * nb;
     return (int)std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)c->nsm * std::max(occ, 1)));
 }

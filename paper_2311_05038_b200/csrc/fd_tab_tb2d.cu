@@ -31,8 +31,8 @@ std::vector<TileCfg> fdtab::tb2d() {
         // r2: 56-column tiles (4096 = 73.1 columns of 56: 74 x 4 chunks = 296
         // CTAs = one wave of two CTAs per SM on C2, vs 64 x 9 = 576 = 1.95 waves)
         make_tb2d<1, 56, 30, 2, 3, 3, 2, 2>(), make_tb2d<1, 56, 30, 2, 2, 3, 2, 2>(),
-        make_tb2d<2, 56, 40, 4, 4, 2, 2, 2>(), make_tb2d<2, 56, 40, 4, 2, 2, 2, 2>(),
-        // r2: one CTA per SM with deep rings (4 stages in flight per SM vs 2)
-        make_tb2d<1, 64, 30, 2, 3, 6, 2, 1>(), make_tb2d<1, 64, 30, 2, 3, 5, 3, 1>(),
-        make_tb2d<2, 64, 40, 4, 4, 4, 2, 1>(), make_tb2d<2, 64, 28, 4, 4, 5, 2, 1>()};
+        make_tb2d<2, 56, 40, 4, 4, 2, 2, 2>(), make_tb2d<2, 56, 40, 4, 2, 2, 2, 2>()};
+        // (r2, removed: one CTA per SM with 5-6-stage rings, 4 stages in flight
+        // per SM instead of 2 -- C2 order 2 418-436 vs 556 Gpts/s, order 4
+        // 281-372 vs 501: 15 warps per SM do not hide the stage latency)
 }

@@ -10,7 +10,8 @@ Covers the fused 3D and 2D kernels (r = 1 and 4, ragged sizes, several
 z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
 naive and unfused reference paths, the two-steps-per-launch kernels
 (3D and 2D, one slab and virtual slabs), the peer-push and sponge variants,
-the per-plane-K (KZ) variants and the cluster-resident kernel.
+the per-plane-K (KZ) variants and the cluster-resident kernel.  With
+FD_TB2D_LINEAR=1 the 2D two-step launches use linear units (r2).
 """
 import os
 import sys
@@ -29,7 +30,7 @@ def main():
         vel = rng.uniform(1500, 2500, dims).astype(np.float32)
         tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3},
               {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_VSLABS: 3}] \
-            if (len(dims) == 2 or order <= 4) else []
+            if (len(dims) == 2 or order <= 4) else [{fd.FD_OPT_TSTEPS: 2}]
         # per-plane K (KZ variants) needs a layered model: the first half of
         # the planes at one velocity, the rest at another
         kz = [{fd.FD_OPT_KPLANE: 1, "layered": True}, {fd.FD_OPT_KPLANE: 1, fd.FD_OPT_TSTEPS: 1, "layered": True},

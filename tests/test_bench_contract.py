@@ -58,6 +58,10 @@ def test_our_arm_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     s = d["sustained"]
     assert s["value"] > 0 and s["steps"] >= 40
+    r = d["repetitions"]
+    assert r["n"] == 5 and len(r["ms"]) == 5 and r["value_min"] <= d["value"] <= r["value_max"]
+    assert abs(d["ms_per_step"] - r["ms_per_step_median"]) < 1e-12
+    assert isinstance(d["gpu_launches"], int) and d["config"]["graph_steps"] > 0
 
 
 def test_gpus_flag_spawns_ranks_launch_check():

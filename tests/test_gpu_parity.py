@@ -548,9 +548,24 @@ def test_tb2d_linear_units_cross_columns(fd, oracle, dims, order):
     nz, nx = dims
     src = [((nz // 2, 64), 25.0, 0.02, 1.0), ((30, 127), 18.0, 0.03, -0.6), ((nz - 40, nx // 2), 12.0, 0.04, 0.5)]
     recs = [(nz // 2 + 1, x) for x in range(0, nx, 3)] + [(z, 128) for z in range(0, nz, 2)] + [(29, 63), (30, 64)]
+    import os
     ref = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 1})
-    lin = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 2})
     chk = run_gpu(fd, vel, h, dt, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3})
+    # the linear split is opt-in (FD_TB2D_LINEAR=1, read once per process): run it in a child
+    import subprocess
+    import sys
+    code = (f"import numpy as np, sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(__file__)))}); "
+            "sys.path.insert(0, sys.argv[1]); import test_gpu_parity as t, paper_2311_05038_b200 as fd; "
+            f"vel = t._rand_vel({dims!r}, seed=83); "
+            f"r = t.run_gpu(fd, vel, {h}, {dt}, {order}, 37, {src!r}, {recs!r}, options={{fd.FD_OPT_TSTEPS: 2}}); "
+            "np.savez(sys.argv[2], P=r[0], Pp=r[1], T=r[2], spl=r[3]['steps_per_launch'], ctas=r[3]['ctas'])")
+    import tempfile
+    out = os.path.join(tempfile.mkdtemp(), "lin.npz")
+    res = subprocess.run([sys.executable, "-c", code, os.path.dirname(__file__), out],
+                         env={**os.environ, "FD_TB2D_LINEAR": "1"}, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-3000:]
+    z = np.load(out)
+    lin = (z["P"], z["Pp"], z["T"], {"steps_per_launch": int(z["spl"])})
     assert lin[3]["steps_per_launch"] == 2
     for a, b, c in zip(lin[:3], chk[:3], ref[:3]):
         assert np.array_equal(a, c) and np.array_equal(b, c)
