@@ -589,17 +589,25 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
     # plane (--kplane, FD_OPT_KPLANE active) 4 B less (K is not streamed)
     kz = bool(info.get("kplane"))
     npts_local = int(np.prod([d for d in info["local_dims"][:wl.ndim]]))     # this rank's points
-    bytes_per_launch = ((20.0 if steps_per_launch == 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * npts_local
+    bytes_per_launch = ((20.0 if steps_per_launch >= 2 else BYTES_PER_POINT) - (4.0 if kz else 0.0)) * npts_local
     achieved = bytes_per_launch / k_avg_s / 1e9
+    if world == 1 and steps_per_launch >= 2 and args.steps % steps_per_launch:
+        # K not a multiple of the steps per launch: the remainder runs as single
+        # steps (16 B per point); the whole region's algorithmic bytes / its time
+        nrem = args.steps % steps_per_launch
+        total = (args.steps // steps_per_launch) * bytes_per_launch + nrem * (BYTES_PER_POINT - (4.0 if kz else 0.0)) * npts_local
+        achieved = total / (ms_step * args.steps / 1e3) / 1e9
     roof = {"bound": "latency" if resident else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": _ncu_traffic(wl.name, wl.order, (":tb2" if steps_per_launch == 2 else "") + (":kz" if kz else "")),
+            "traffic": _ncu_traffic(wl.name, wl.order, (f":tb{steps_per_launch}" if steps_per_launch >= 2 else "")
+                                    + (":kz" if kz else "")),
             "peak_source": peak_src,
             "algorithmic_bytes_per_point": bytes_per_launch / npts_local / steps_per_launch,
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
             "points_per_launch": npts_local,
             "kernel": "resident_kernel" if resident else
                       {(3, 1): "fused_step_kernel", (3, 2): "tb2ws_step_kernel", (2, 1): "tile2d_step_kernel",
-                       (2, 2): "tb2d_step_kernel"}[(wl.ndim, steps_per_launch)],
+                       (2, 2): "tb2d_step_kernel", (2, 3): "tbs2d_step_kernel",
+                       (2, 4): "tbs2d_step_kernel"}[(wl.ndim, steps_per_launch)],
             "kernel_ms_per_launch": k_avg_s * 1e3, "launches_per_pass": kn / max(npass, 1),
             "kernel_ms_per_launch_profile_pass": k_avg_prof_s * 1e3,
             "kernel_share_of_step_profile_pass": (kms / max(sum(v[0] for v in ktimes.values()), 1e-12))
@@ -663,8 +671,9 @@ def main(argv=None):
                     help="absorbing Cerjan frame of this many cells (fd_set_sponge, alpha 0.015); 0 = band rule only")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="halo transport at N>1: NCCL send/recv or in-kernel peer stores (CUDA IPC)")
-    ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2],
-                    help="0 auto (library default), 1 one step per launch, 2 temporal blocking (10 B/update)")
+    ap.add_argument("--tsteps", type=int, default=0, choices=[0, 1, 2, 3, 4],
+                    help="0 auto (library default), 1 one step per launch, S >= 2 temporal blocking "
+                         "(S steps per launch, 20/S B per update; S >= 3: 2D single slab)")
     ap.add_argument("--sustained", type=float, default=2.0,
                     help="seconds of an extra graph-replay pass reported as 'sustained' (power-capped state); 0 = off")
     ap.add_argument("--strong", action="store_true",

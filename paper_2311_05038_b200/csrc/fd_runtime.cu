@@ -116,7 +116,7 @@ static const std::vector<TileCfg> &tile_table() {
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = [] {
         std::vector<TileCfg> v;
-        for (auto part : {fdtab::tb2ws, fdtab::tb2d}) {
+        for (auto part : {fdtab::tb2ws, fdtab::tb2d, fdtab::tbs2d}) {
             auto p = part();
             v.insert(v.end(), p.begin(), p.end());
         }
@@ -250,7 +250,7 @@ struct fd_ctx {
     // kernel configuration
     int opt_kernel = 0, opt_tile = -1, opt_zchunks = 0, opt_async = 0, opt_graph = 1, opt_vslabs = 1;
     int opt_profile = 0;
-    int opt_tsteps = 0;                   // 0 auto, 1 single steps, 2 temporal blocking (two steps/launch)
+    int opt_tsteps = 0;                   // 0 auto, 1 single steps, S >= 2 temporal blocking (S steps/launch)
     int opt_tb2tile = -1;
     int tb2 = -1, tb2occ = 0;             // chosen tb2_table() entry
     // FD_OPT_RESIDENT: whole fd_step calls in one cluster launch (fd_resident.cuh)
@@ -612,7 +612,7 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
         const double len = (double)span / (double)cc;
         // ~half the 2r warm-up planes' cost (3D); the A -> B lag of one row
         // block per chunk (2D two-step)
-        const double warm = c->ndim == 3 ? c->R : (tb2d ? (double)t.ty : 0.0);
+        const double warm = c->ndim == 3 ? c->R : (tb2d ? (double)t.ty * (t.steps - 1) : 0.0);
         const double score = fill * len / (len + warm);
         if (score > bscore + 1e-9) { bscore = score; best = cc; }
     }
@@ -1013,24 +1013,32 @@ static fd_status prepare(fd_ctx *c) {
             }
         }
         // single steps between temporal-blocking launches refresh 2r halo planes
-        const int32_t bw = c->opt_tsteps == 2 ? c->H : c->R;
+        const int32_t bw = c->opt_tsteps >= 2 ? c->H : c->R;
         split_regions(c, s, overlap, bw, c->opt_kernel != 0 ? nullptr : &tile_table()[c->tile], c->occ, s.regions);
         for (auto &g : s.regions) {
             st = upload_region_receivers(c, s, g, c->opt_kernel != 0 ? nullptr : &tile_table()[c->tile]);
             if (st) return st;
         }
     }
-    if (c->opt_tsteps == 2) {
-        // temporal blocking (3D orders 2-8, 2D), fused path
-        if (c->opt_kernel != 0) return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=2 needs the fused kernel");
+    if (c->opt_tsteps >= 2) {
+        // temporal blocking: 2 steps per launch (3D orders 2-8, 2D; slabs, ranks,
+        // sponge, peer pushes), S >= 3 (2D single-slab band-rule contexts)
+        if (c->opt_kernel != 0) return fail(FD_ERR_STATE, "FD_OPT_TSTEPS >= 2 needs the fused kernel");
+        if (c->opt_tsteps >= 3 && (c->ndim != 2 || multi || c->sponge_nb > 0 || c->opt_transport == 1))
+            return fail(FD_ERR_STATE, "FD_OPT_TSTEPS=%d: 2D single-slab contexts without the sponge frame",
+                        c->opt_tsteps);
         const auto &tb = tb2_table();
         for (int i = 0; i < (int)tb.size() && c->tb2 < 0; ++i) {
-            if (tb[i].r != c->R || tb[i].ndim != c->ndim || (c->opt_tb2tile >= 0 && i != c->opt_tb2tile)) continue;
+            if (tb[i].r != c->R || tb[i].ndim != c->ndim || tb[i].steps != c->opt_tsteps ||
+                (c->opt_tb2tile >= 0 && i != c->opt_tb2tile))
+                continue;
             if (needs_full(c) && !tb[i].full()) continue;
             const int occ = occupancy(c, tb[i]);
             if (occ > 0) { c->tb2 = i; c->tb2occ = occ; }
         }
-        if (c->tb2 < 0) return fail(FD_ERR_CUDA, "no temporal-blocking configuration fits this device");
+        if (c->tb2 < 0)
+            return fail(c->opt_tsteps >= 3 ? FD_ERR_STATE : FD_ERR_CUDA,
+                        "no %d-steps-per-launch configuration for this order / device", c->opt_tsteps);
         const TileCfg &t = tb[c->tb2];
         for (int v = 0; v < kVariants; ++v)
             if (t.kernel[v])
@@ -1096,7 +1104,7 @@ static fd_status prepare(fd_ctx *c) {
     // per-plane K once K and its halos are final (peer-transport ranks receive
     // K's halos with the first exchange: they keep the K field)
     const bool kz_compiled = c->tile >= 0 && tile_table()[c->tile].full() &&
-                             (c->opt_tsteps != 2 || (c->tb2 >= 0 && tb2_table()[c->tb2].full()));
+                             (c->opt_tsteps < 2 || (c->tb2 >= 0 && tb2_table()[c->tb2].full()));
     if (c->opt_kplane && c->opt_kernel == 0 && !c->resident && !(c->nranks > 1 && c->opt_transport == 1) &&
         kz_compiled) {
         st = build_kplane(c);
@@ -1331,7 +1339,7 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     const CUtensorMap &mp = s.mHalo[c->icur];
     const CUtensorMap &mpp = s.mTile[c->iprev];
     const bool push = c->opt_transport == 1 && g.boundary;
-    if (push) set_push(c, s, p, c->iprev, c->opt_tsteps == 2 ? c->H : c->R, -1, 0);
+    if (push) set_push(c, s, p, c->iprev, c->opt_tsteps >= 2 ? c->H : c->R, -1, 0);
     const launch_fused_t go = t.launch[(c->d_gsp ? kVarSponge : 0) | (push ? kVarPeer : 0) | (c->kplane ? kVarKPlane : 0)];
     tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, mp, mpp, s.mK, p); });
 }
@@ -1494,7 +1502,7 @@ static fd_status one_step(fd_ctx *c) {
                 if (g.boundary) launch_region(c, sl, g, c->comm_stream);
         if (peer_ranks) peer_signal(c, c->comm_stream);
         if (c->opt_transport != 1) {
-            const int d = c->opt_tsteps == 2 ? c->H : c->R;     // = the boundary regions' width
+            const int d = c->opt_tsteps >= 2 ? c->H : c->R;     // = the boundary regions' width
             tracked(c, FD_K_HALO, c->comm_stream, [&] { s = exchange(c, {{c->iprev, d}}, c->comm_stream); },
                     false);
             if (s) return s;
@@ -1510,7 +1518,7 @@ static fd_status one_step(fd_ctx *c) {
         if (c->slabs.size() > 1 || c->nranks > 1) {
             // the new P (a single step between temporal-blocking launches
             // needs all 2r halo planes; the new P_prev keeps its valid ones)
-            const int d = c->opt_tsteps == 2 ? c->H : c->R;
+            const int d = c->opt_tsteps >= 2 ? c->H : c->R;
             tracked(c, FD_K_HALO, c->stream, [&] { s = exchange(c, {{c->iprev, d}}, c->stream); }, false);
             if (s) return s;
         }
@@ -1547,7 +1555,9 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, m0, mm, s.mKe, p); });
 }
 
-static fd_status two_steps(fd_ctx *c) {
+// S steps per launch (S = 2: tb2ws / tb2d; S >= 3: tbs2d, single slab).
+static fd_status tb_steps(fd_ctx *c) {
+    const int S = tb2_table()[c->tb2].steps;
     int f1 = -1, f2 = -1;
     for (int b = 0; b < 4; ++b)
         if (b != c->icur && b != c->iprev) (f1 < 0 ? f1 : f2) = b;
@@ -1578,27 +1588,32 @@ static fd_status two_steps(fd_ctx *c) {
     CUDA_TRY(c, cudaGetLastError());
     c->iprev = f1;
     c->icur = f2;
-    c->k += 2;
+    c->k += S;
     return FD_OK;
 }
 
 // Advance m steps with plain launches (pairs through temporal blocking).
 static fd_status advance_plain(fd_ctx *c, int64_t m) {
-    const bool tb = c->opt_tsteps == 2 && c->tb2 >= 0;
+    const int S = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].steps : 1;
     while (m > 0) {
-        fd_status s = (tb && m >= 2) ? two_steps(c) : one_step(c);
+        fd_status s = (S >= 2 && m >= S) ? tb_steps(c) : one_step(c);
         if (s) return s;
-        m -= (tb && m >= 2) ? 2 : 1;
+        m -= (S >= 2 && m >= S) ? S : 1;
     }
     return FD_OK;
 }
 
 // ------------------------------------------------------------ CUDA graphs
-// kGraphSteps consecutive steps captured once per starting buffer parity and
+// graph_len(c) consecutive steps captured once per starting buffer parity and
 // replayed (launch-bound small grids).  Kernels read k = *d_k + offset; the
 // graph ends by advancing d_k.  Not used while profiling, nor with the peer
 // transport across ranks (its flag waits carry per-exchange counts).
-constexpr int64_t kGraphSteps = 16;
+// steps per graph: a multiple of the steps per launch (24 for three-step
+// launches, else 16), so no graph holds a single-step remainder launch
+static int64_t graph_len(const fd_ctx *c) {
+    const int S = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].steps : 1;
+    return S == 3 ? 24 : 16;
+}
 
 static bool graphs_usable(const fd_ctx *c) {
     // virtual slabs: the two-stream schedule is captured too (event fork/join).
@@ -1612,7 +1627,7 @@ static bool graphs_usable(const fd_ctx *c) {
     return c->opt_graph && ranks_ok && !c->opt_profile && c->d_k && c->stream && !c->resident;
 }
 
-// Capture kGraphSteps steps starting from the current buffer roles; the
+// Capture graph_len(c) steps starting from the current buffer roles; the
 // entry records the roles it ends in.  Returns the entry index or -1.
 static int capture_graph(fd_ctx *c, fd_status *st) {
     const int64_t k0 = c->k, l0 = c->launches;
@@ -1623,8 +1638,8 @@ static int capture_graph(fd_ctx *c, fd_status *st) {
     if (e != cudaSuccess) { cudaGetLastError(); c->opt_graph = 0; return -1; }
     c->capturing = true;
     c->gk0 = k0;
-    fd_status s = advance_plain(c, kGraphSteps);
-    advance_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, kGraphSteps);
+    fd_status s = advance_plain(c, graph_len(c));
+    advance_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, graph_len(c));
     c->capturing = false;
     e = cudaStreamEndCapture(c->stream, &graph);
     fd_ctx::Graph gr{ic0, ip0, c->icur, c->iprev, nullptr, c->d_traces, c->d_wtab, c->launches - l0 + 1};
@@ -1658,7 +1673,7 @@ static fd_status reserve_steps(fd_ctx *c, int64_t n) {
     }
     s = ensure_tables(c, c->k + n);
     if (s) return s;
-    if (graphs_usable(c) && n >= kGraphSteps) {
+    if (graphs_usable(c) && n >= graph_len(c)) {
         int ic = c->icur, ip = c->iprev;
         for (int guard = 0; guard < 8; ++guard) {
             const int sic = c->icur, sip = c->iprev;
@@ -1793,14 +1808,14 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         }
         if (c->nranks > 1 && c->opt_transport == 1) {
             // peer transport: push the initial halos (and K's, once) with copies
-            if (c->opt_tsteps == 2) s = peer_copy(c, {{c->icur, c->H}, {c->iprev, c->R}, {-1, c->R}}, c->stream);
+            if (c->opt_tsteps >= 2) s = peer_copy(c, {{c->icur, c->H}, {c->iprev, c->R}, {-1, c->R}}, c->stream);
             else s = peer_copy(c, {{c->icur, c->R}}, c->stream);
             if (s) return s;
             peer_signal(c, c->stream);
         } else if (c->slabs.size() > 1 || c->nranks > 1) {
             // halos of P (2r for temporal blocking) and, for temporal
             // blocking, r of P_prev (fd_set_wavefield may have set it)
-            if (c->opt_tsteps == 2) s = exchange(c, {{c->icur, c->H}, {c->iprev, c->R}}, c->stream);
+            if (c->opt_tsteps >= 2) s = exchange(c, {{c->icur, c->H}, {c->iprev, c->R}}, c->stream);
             else s = exchange(c, {{c->icur, c->R}}, c->stream);
             if (s) return s;
         }
@@ -1812,11 +1827,11 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         if (s) return s;
         i = n;
     }
-    if (graphs_usable(c) && n - i >= kGraphSteps) {
+    if (graphs_usable(c) && n - i >= graph_len(c)) {
         // replay G-step graphs; the device counter d_k carries k
         set_step_kernel<<<1, 1, 0, c->stream>>>(c->d_k, c->k);
         ++c->launches;
-        for (; n - i >= kGraphSteps; i += kGraphSteps) {
+        for (; n - i >= graph_len(c); i += graph_len(c)) {
             int gi = -1;
             for (size_t q = 0; q < c->graphs.size(); ++q) {
                 auto &g = c->graphs[q];
@@ -1836,8 +1851,8 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
             }
             auto &g = c->graphs[gi];
             CUDA_TRY(c, cudaGraphLaunch(g.exec, c->stream));
-            c->k += kGraphSteps;
-            c->graph_steps += kGraphSteps;
+            c->k += graph_len(c);
+            c->graph_steps += graph_len(c);
             c->icur = g.end_icur;
             c->iprev = g.end_iprev;
             c->launches += g.launches;
@@ -2138,7 +2153,7 @@ fd_status fd_set_option(fd_ctx *c, int key, int64_t v) {
         c->opt_zchunks = (int)v;
         return FD_OK;
     case FD_OPT_TSTEPS:
-        if (v < 0 || v > 2) return fail(FD_ERR_ARG, "FD_OPT_TSTEPS must be 0 (auto), 1 or 2");
+        if (v < 0 || v > 4) return fail(FD_ERR_ARG, "FD_OPT_TSTEPS must be 0 (auto), 1, 2, 3 or 4");
         c->opt_tsteps = (int)v;
         return FD_OK;
     case FD_OPT_TB2TILE:
@@ -2204,7 +2219,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->pitch = c->pitch;
     o->order = c->order;
     o->device_bytes = c->dev_bytes;
-    o->steps_per_launch = (c->opt_tsteps == 2) ? 2 : 1;
+    o->steps_per_launch = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].steps : 1;
     o->kplane = c->kplane ? 1 : 0;
     o->graph_steps = c->graph_steps;
     if (c->comm && nccl().CommCount) {
@@ -2219,7 +2234,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
         o->ctas = c->res_nc; o->threads_per_cta = c->res_threads; o->smem_bytes = c->res_smem;
         return FD_OK;
     }
-    if (c->opt_tsteps == 2 && c->tb2 >= 0) {
+    if (c->opt_tsteps >= 2 && c->tb2 >= 0) {
         const TileCfg &t = tb2_table()[c->tb2];
         o->tile_x = t.tx; o->tile_y = t.ty; o->rows_per_thread = t.ny;
         o->p_stages = 2 * t.r + 1 + t.dp; o->k_stages = t.r + 1 + t.dk;

@@ -30,6 +30,7 @@ struct TileCfg {
     int threads, smem;
     const void *kernel[kVariants];
     launch_fused_t launch[kVariants];
+    int steps = 2;       // time steps per launch (temporal-blocking table: 2, or S of tbs2d)
     bool full() const { return kernel[kVariants - 1] != nullptr; }
 };
 
@@ -39,6 +40,7 @@ std::vector<TileCfg> tiles3d_r34();   // fused_step_kernel, r = 3, 4   (fd_tab_3
 std::vector<TileCfg> tiles2d();       // tile2d_step_kernel           (fd_tab_2d.cu)
 std::vector<TileCfg> tb2ws();         // tb2ws_step_kernel, 3D r <= 2  (fd_tab_tb2ws.cu)
 std::vector<TileCfg> tb2d();          // tb2d_step_kernel, 2D          (fd_tab_tb2d.cu)
+std::vector<TileCfg> tbs2d();         // tbs2d_step_kernel, 2D, S >= 3 (fd_tab_tbs.cu)
 }  // namespace fdtab
 
 #ifdef FD_TABLE_TU

@@ -126,3 +126,16 @@ def test_package_fails_loudly_without_the_library(tmp_path):
             % str(tmp_path))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120).stdout
     assert "IMPORTERROR" in out and "libfd.so is missing" in out and "no CPU fallback" in out
+
+
+def test_plane_too_large_for_32bit_offsets(fd):
+    """The step kernels keep in-plane offsets in 32 bits: a 3D plane of
+    47000 x 47000 points (8 planes: ~70 GB, would fit a B200) is refused with
+    FD_ERR_ARG before the model is read (a 1-float buffer is passed)."""
+    dims = np.asarray((8, 47000, 47000), np.int64)
+    v = np.full(1, 2000.0, np.float32)
+    ctx = ctypes.c_void_p()
+    st = fd.lib.fd_create(ctypes.byref(ctx), 3, dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 10.0, 1e-3, 2,
+                          v.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), 0)
+    assert st == fd.FD_ERR_ARG and not ctx.value
+    assert b"32-bit" in fd.lib.fd_last_error()

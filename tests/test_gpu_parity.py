@@ -536,6 +536,70 @@ def test_temporal_blocking_2d_bitwise(fd, oracle, dims, order):
     assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
 
 
+@pytest.mark.parametrize("dims,order,tsteps", [((90, 300), 2, 3), ((200, 517), 2, 3), ((131, 200), 2, 4),
+                                               ((333, 700), 2, 4), ((131, 200), 4, 3), ((260, 613), 4, 3)])
+def test_tbs2d_s_steps_bitwise(fd, oracle, dims, order, tsteps):
+    """S steps per launch (2D, S = 3, 4; fd_tbs.cuh): bitwise equal to single
+    steps for every compiled S-step configuration, z-chunk counts and graph
+    on/off, across fd_step calls of lengths that are not multiples of S (the
+    remainder runs as single steps), with sources on block / column faces,
+    two sources on one point, a source in the band, and receivers at sources,
+    in the band and on block faces; and the oracle within 1e-4."""
+    from paper_2311_05038_b200 import fd as fdm
+    vel = _rand_vel(dims, seed=89)
+    h, dt = 10.0, 0.5e-3
+    nz, nx = dims
+    r = order // 2
+    src = [((nz // 2, nx // 2), 25.0, 0.02, 1.0), ((30, 64), 18.0, 0.03, -0.6), ((nz // 2, nx // 2), 12.0, 0.04, 0.3),
+           ((r - 1, 70), 20.0, 0.025, 0.2), ((59, 127), 15.0, 0.03, 0.4)]
+    recs = [(nz // 2, nx // 2), (29, 63), (30, 64), (nz - 3, 5), (1, 1), (60, 130 % nx), (59, 128), (0, 70)]
+    seq = (1, 7, 24, 2, 13)
+    P0 = np.random.default_rng(97).standard_normal(dims).astype(np.float32) * 1e-3
+
+    def run(options):
+        with fd.Simulation(vel, h, dt, order, options=tiled(fd, options)) as sim:
+            sim.set_wavefield(fd.FD_FIELD_CUR, P0)
+            for sdef in src:
+                sim.add_source(*sdef)
+            sim.set_receivers(recs)
+            for n in seq:
+                sim.step(n)
+            return sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces(), sim.info()
+
+    ref = run({fd.FD_OPT_TSTEPS: 1})
+    ntb = 0
+    for tile in range(64):
+        for zc in (0, 1, 3):
+            for graph in (1, 0):
+                try:
+                    got = run({fd.FD_OPT_TSTEPS: tsteps, fdm.FD_OPT_TB2TILE: tile, fd.FD_OPT_ZCHUNKS: zc,
+                               fd.FD_OPT_GRAPH: graph})
+                except fdm.FDError as e:
+                    assert e.status in (-1, -5, -7), e
+                    break
+                assert got[3]["steps_per_launch"] == tsteps
+                ntb += 1
+                for a, b in zip(got[:3], ref[:3]):
+                    assert np.array_equal(a, b), (tile, zc, graph)
+    assert ntb >= 2
+    Po, Ppo, To = oracle.run(vel, h, dt, order, sum(seq), src, recs, P0=P0, nthreads=4)
+    assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[1], Ppo) <= TOL and rel_l2(ref[2], To) <= TOL
+
+
+def test_tbs2d_refuses_unsupported_contexts(fd):
+    vel3 = _rand_vel((30, 30, 40), seed=3)
+    vel2 = _rand_vel((100, 200), seed=3)
+    cases = [(vel3, 2, {fd.FD_OPT_TSTEPS: 3}, None), (vel2, 2, {fd.FD_OPT_TSTEPS: 3, fd.FD_OPT_VSLABS: 2}, None),
+             (vel2, 2, {fd.FD_OPT_TSTEPS: 3}, (6, 0.05)), (vel2, 8, {fd.FD_OPT_TSTEPS: 3}, None)]
+    for vel, order, opts, sponge in cases:
+        with pytest.raises(fd.FDError) as e:
+            with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd, opts)) as sim:
+                if sponge:
+                    sim.set_sponge(*sponge)
+                sim.step(3)
+        assert e.value.status == fd.FD_ERR_STATE, (opts, e.value)
+
+
 @pytest.mark.parametrize("dims,order", [((600, 1100), 2), ((517, 1000), 4), ((430, 900), 8)])
 def test_tb2d_linear_units_cross_columns(fd, oracle, dims, order):
     """2D two-step launches split the row blocks into one wave of contiguous

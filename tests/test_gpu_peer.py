@@ -68,10 +68,14 @@ def test_peer_virtual_slabs_bitwise(fd, oracle, dims, order, nslabs, tsteps):
     assert rel_l2(got[0], Po) <= TOL and rel_l2(got[1], Ppo) <= TOL and rel_l2(got[2], To) <= TOL
 
 
-def test_peer_transport_needs_slabs(fd):
+@pytest.mark.parametrize("resident", [1, 0])
+def test_peer_transport_needs_slabs(fd, resident):
+    """FD_OPT_TRANSPORT=1 on a single-slab context fails at the first step --
+    also where the auto policy would pick the cluster-resident path (a small
+    grid, FD_OPT_RESIDENT left at auto: ADVICE r1)."""
     vel = _rand_vel((20, 20, 20), seed=1)
     with pytest.raises(fd.FDError) as e:
-        with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_TRANSPORT: 1, fd.FD_OPT_RESIDENT: 1}) as sim:
+        with fd.Simulation(vel, 10.0, 1e-3, 2, options={fd.FD_OPT_TRANSPORT: 1, fd.FD_OPT_RESIDENT: resident}) as sim:
             sim.step(1)
     assert e.value.status == fd.FD_ERR_STATE
 
