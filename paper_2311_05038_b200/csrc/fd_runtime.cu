@@ -1009,6 +1009,8 @@ static fd_status prepare(fd_ctx *c) {
                 if (a == 1 && c->ndim == 2) continue;
                 s.D[a] = (float *)dev_alloc(db);
                 if (!s.D[a]) return fail(FD_ERR_NOMEM, "derivative field allocation failed");
+                // the pitch padding is never written but read by fd_time's edge quads
+                CUDA_TRY(c, cudaMemset(s.D[a], 0, db));
                 c->dev_bytes += (double)db;
             }
         }

@@ -11,7 +11,7 @@ TAG=${TAG:-r03}
 SPECS=${SPECS:-"C3:2:2 C3:2:1 C3:8:1"}
 for spec in $SPECS; do
   IFS=: read cfg ord ts kz <<< "$spec"
-  sfx=""; [ "$ts" = "2" ] && sfx="_tb2"
+  sfx=""; [ "$ts" -ge 2 ] && sfx="_tb${ts}"
   kzf=""; [ "${kz:-}" = "kz" ] && { sfx="${sfx}_kz"; kzf="--kplane"; }
   # launch list (cold-cache, serialised): compare the step kernel's SHARE of the step
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \

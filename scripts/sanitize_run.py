@@ -31,6 +31,10 @@ def main():
         tb = [{fd.FD_OPT_TSTEPS: 2}, {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_ZCHUNKS: 3},
               {fd.FD_OPT_TSTEPS: 2, fd.FD_OPT_VSLABS: 3}] \
             if (len(dims) == 2 or order <= 4) else [{fd.FD_OPT_TSTEPS: 2}]
+        if len(dims) == 2 and order <= 4:          # S steps per launch (fd_tbs.cuh)
+            tb += [{fd.FD_OPT_TSTEPS: 3}, {fd.FD_OPT_TSTEPS: 3, fd.FD_OPT_ZCHUNKS: 3}]
+            if order == 2:
+                tb += [{fd.FD_OPT_TSTEPS: 4}]
         # per-plane K (KZ variants) needs a layered model: the first half of
         # the planes at one velocity, the rest at another
         kz = [{fd.FD_OPT_KPLANE: 1, "layered": True}, {fd.FD_OPT_KPLANE: 1, fd.FD_OPT_TSTEPS: 1, "layered": True},
