@@ -69,13 +69,16 @@ def main(tag):
              "launch of the fused step kernel; launch lists with gpu__time_duration.sum).  Algorithmic bytes",
              "= 16 B x grid points per launch (DESIGN.md section 5.4).", ""]
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
-        m = re.match(rf"prof_{tag}_(C\d)_o(\d)(_tb2)?(_kz)?\.ncu-rep", os.path.basename(rep))
+        m = re.match(rf"prof_{tag}_(C\d)_o(\d)(_tb(\d))?(_kz)?\.ncu-rep", os.path.basename(rep))
         if not m:
             continue
-        wl, order, tb2, kz = m.group(1), int(m.group(2)), bool(m.group(3)), bool(m.group(4))
+        wl, order, kz = m.group(1), int(m.group(2)), bool(m.group(5))
+        spl = int(m.group(4)) if m.group(4) else 1
         d = raw(rep)
         kname = d.get("Kernel Name", ("", ""))[0]
-        tb2 = tb2 or "tb2" in kname          # the default 3D order-2 path is two steps per launch
+        if spl == 1 and "tb2" in kname:      # the default 3D order-2 path is two steps per launch
+            spl = 2
+        tb2 = spl >= 2
         rd = to_bytes(*d["dram__bytes_read.sum"])
         wr = to_bytes(*d["dram__bytes_write.sum"])
         npts = npts_of(wl)
@@ -83,10 +86,10 @@ def main(tag):
         dunit = d["gpu__time_duration.sum"][1]
         dur_s = dur * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-9)
         alg = ((20.0 if tb2 else 16.0) - (4.0 if kz else 0.0)) * npts    # K per plane: not streamed
-        summ[f"{wl}:o{order}{':tb2' if tb2 else ''}{':kz' if kz else ''}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+        summ[f"{wl}:o{order}{f':tb{spl}' if tb2 else ''}{':kz' if kz else ''}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                   "algorithmic_bytes": alg, "bytes_per_point": (rd + wr) / npts,
                                   "ncu_duration_s": dur_s, "tag": tag}
-        lines += [f"## {wl}, order {order}{' (temporal blocking, 2 steps per launch)' if tb2 else ''}"
+        lines += [f"## {wl}, order {order}{f' (temporal blocking, {spl} steps per launch)' if tb2 else ''}"
                   f"{' (K per plane, FD_OPT_KPLANE)' if kz else ''}", "",
                   f"* kernel: `{kname[:120]}`",
                   f"* DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB = {(rd + wr) / npts:.2f} B/pt "
