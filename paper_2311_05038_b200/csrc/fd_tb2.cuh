@@ -68,6 +68,11 @@ __device__ __forceinline__ void role_release(B *...bars) {
 #ifndef FD_XSHFL_3D
 #define FD_XSHFL_3D 0
 #endif
+// FD_TB2_COLQ: the y-tap column takes the thread's own rows from its z queue
+// (1) instead of re-reading them from shared memory (0)
+#ifndef FD_TB2_COLQ
+#define FD_TB2_COLQ 1
+#endif
 template <int R, bool SHFL>
 __device__ __forceinline__ void quad_xtaps(float (&av)[12], const float4 M4, const float *lq, bool needL, bool needR) {
     av[4] = M4.x; av[5] = M4.y; av[6] = M4.z; av[7] = M4.w;
@@ -276,12 +281,13 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float4 oraw[C::NYA];                                  // raw P^{k+1} (receivers)
 #pragma unroll
             for (int yy = 0; yy < C::NYA; ++yy) oraw[yy] = make_float4(0.f, 0.f, 0.f, 0.f);
-            {   // all lanes (inactive ones compute on row 0 / quad 0 and store nothing): the x taps shuffle
+            // shuffled x taps need every lane (inactive ones compute on row 0 / quad 0 and store nothing)
+            if (FD_XSHFL_3D == 1 || FD_XSHFL_3D == 3 || act) {
                 float4 col[C::NYA + 2 * R];       // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
                 for (int i = 0; i < C::NYA + 2 * R; ++i)
-                    col[i] = (i >= R && i < R + C::NYA) ? qz[(PH + R) % Q][i - R]
-                                                        : lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
+                    col[i] = (FD_TB2_COLQ && i >= R && i < R + C::NYA) ? qz[(PH + R) % Q][i - R]
+                                                                      : lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
                     const int re = re0 + yy;
@@ -430,12 +436,12 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         const float sgz = SP ? sponge_gz(prm, gz) : 1.f;
         const float kzb = KZ ? kplane(prm, z2) : 0.f;
         float4 out[C::NYB];
-        {   // all lanes (inactive ones compute on row 0 and store nothing): the x taps shuffle
+        if (FD_XSHFL_3D == 1 || FD_XSHFL_3D == 2 || act) {   // (shuffles: every lane)
             float4 col[C::NYB + 2 * R];           // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
             for (int i = 0; i < C::NYB + 2 * R; ++i)
-                col[i] = (i >= R && i < R + C::NYB) ? qz[(PH + R) % Q][i - R]
-                                                    : lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
+                col[i] = (FD_TB2_COLQ && i >= R && i < R + C::NYB) ? qz[(PH + R) % Q][i - R]
+                                                                  : lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy) {
                 const int re = ri0 + yy + R;

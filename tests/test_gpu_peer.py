@@ -148,3 +148,25 @@ def test_bench_two_ranks_peer_transport_shared_gpu(fd, strong):
     assert d["scaling"] == ("strong" if strong else "weak")
     assert d["roofline"]["points_per_launch"] == (d["config"]["grid"][0] // (2 if strong else 1)) * d["config"]["grid"][1]
     assert "peer" in d["config"]["parallelism"] and d["config"]["shared_gpu"]
+
+
+def test_nccl_init_failure_poisons_the_context(fd, tmp_path):
+    """SURVEY T5 (NCCL error propagation): rank 1 of a two-rank context given a
+    unique id whose bootstrap root does not exist -- ncclCommInitRank fails at
+    the first fd_step, which returns FD_ERR_NCCL; the context is poisoned
+    (later calls FD_ERR_STATE) and fd_destroy still succeeds.  Run in a child
+    process (NCCL retries the connection for a few seconds)."""
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1])\n"
+        "import paper_2311_05038_b200 as fd\n"
+        "vel = np.full((40, 64), 2000.0, np.float32)\n"
+        "ctx = fd.fd_create_dist(vel, (80, 64), 10.0, 1e-3, 2, 1, 2, 0, bytes(128), True)\n"
+        "try:\n    fd.fd_step(ctx, 1)\n    print('NOERROR')\n"
+        "except fd.FDError as e:\n    print('STEP', e.status)\n"
+        "try:\n    fd.fd_step(ctx, 1)\nexcept fd.FDError as e:\n    print('AGAIN', e.status)\n"
+        "fd.fd_destroy(ctx)\nprint('DESTROYED')\n")
+    env = {**os.environ, "NCCL_SOCKET_IFNAME": "lo", "NCCL_DEBUG": "WARN"}
+    res = subprocess.run([sys.executable, "-c", code, ROOT], env=env, capture_output=True, text=True, timeout=300)
+    out = res.stdout
+    assert f"STEP {fd.FD_ERR_NCCL}" in out, out + res.stderr[-2000:]
+    assert f"AGAIN {fd.FD_ERR_STATE}" in out and "DESTROYED" in out, out
