@@ -603,9 +603,15 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     const bool tb2d = c->ndim == 2 && c->tb2 >= 0 && &t == &tb2_table()[c->tb2];
     const int64_t waves_target = c->ndim == 3 ? 6 : (tb2d ? 2 : 3);
     const int64_t target = std::max<int64_t>(1, (waves_target * slots + ntiles / 2) / ntiles);
+    // 3D: z-chunks of at most 128 planes.  The co-resident CTAs of a wave
+    // stream neighbouring tiles through z in step and share their x-y halos
+    // in L2; over longer chunks they drift apart and the halos come from DRAM
+    // again (r2, C4 1024^3 two-step: 2 chunks of 512 planes 572 Gpts/s with
+    // 14.3 GB read per launch, 8 chunks of 128 planes 626; C5:1 603 -> 623)
+    const int64_t chmin = c->ndim == 3 ? std::min<int64_t>(chmax, (span + 127) / 128) : 1;
     int64_t best = 1;
     double bscore = -1;
-    for (int64_t ch = std::max<int64_t>(1, target - 3); ch <= target + 3; ++ch) {
+    for (int64_t ch = std::max<int64_t>({(int64_t)1, target - 3, chmin}); ch <= std::max(target, chmin) + 3; ++ch) {
         const int64_t cc = std::min(ch, chmax);
         const int64_t units = ntiles * cc, waves = (units + slots - 1) / slots;
         const double fill = (double)units / (double)(waves * slots);

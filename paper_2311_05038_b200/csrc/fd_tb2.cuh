@@ -69,9 +69,10 @@ __device__ __forceinline__ void role_release(B *...bars) {
 #define FD_XSHFL_3D 0
 #endif
 // FD_TB2_COLQ: the y-tap column takes the thread's own rows from its z queue
-// (1) instead of re-reading them from shared memory (0)
+// instead of re-reading them from shared memory -- bit 0: stage A, bit 1:
+// stage B (3: both)
 #ifndef FD_TB2_COLQ
-#define FD_TB2_COLQ 1
+#define FD_TB2_COLQ 3
 #endif
 template <int R, bool SHFL>
 __device__ __forceinline__ void quad_xtaps(float (&av)[12], const float4 M4, const float *lq, bool needL, bool needR) {
@@ -286,7 +287,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
                 float4 col[C::NYA + 2 * R];       // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
                 for (int i = 0; i < C::NYA + 2 * R; ++i)
-                    col[i] = (FD_TB2_COLQ && i >= R && i < R + C::NYA) ? qz[(PH + R) % Q][i - R]
+                    col[i] = ((FD_TB2_COLQ & 1) && i >= R && i < R + C::NYA) ? qz[(PH + R) % Q][i - R]
                                                                       : lds128(tc + (re0 + i) * C::BX0 + 4 * q + 4);
 #pragma unroll
                 for (int yy = 0; yy < C::NYA; ++yy) {
@@ -440,7 +441,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             float4 col[C::NYB + 2 * R];           // y taps; the thread's own rows are its z-queue centre
 #pragma unroll
             for (int i = 0; i < C::NYB + 2 * R; ++i)
-                col[i] = (FD_TB2_COLQ && i >= R && i < R + C::NYB) ? qz[(PH + R) % Q][i - R]
+                col[i] = ((FD_TB2_COLQ & 2) && i >= R && i < R + C::NYB) ? qz[(PH + R) % Q][i - R]
                                                                   : lds128(t1c + (ri0 + i) * C::BXE + 4 * q);
 #pragma unroll
             for (int yy = 0; yy < C::NYB; ++yy) {
