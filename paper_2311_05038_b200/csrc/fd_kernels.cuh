@@ -275,6 +275,19 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
 }
 __device__ __forceinline__ float4 lds128(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 
+// Programmatic dependent launch (r2, FD_PDL): a step kernel launched with the
+// programmatic-serialization attribute may start while the previous step
+// kernel of the stream drains; everything before this point (barrier init,
+// tensor-map prefetch) overlaps that tail, everything after it (every read
+// of the fields the previous launch wrote, every write of the buffers it
+// reads) waits for the previous grid's completion and memory flush.  The
+// trigger lets the next launch be scheduled once every CTA of this one has
+// started.  Without the attribute griddepcontrol.wait returns at once.
+__device__ __forceinline__ void pdl_sync() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float f4(const float4 &v, int e) {
     return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
@@ -493,6 +506,7 @@ fused_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, box
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_sync();
     if (z1 <= z0) return;
 
     // Load l = 0 .. nload-1 brings p plane j = z0 - R + l (buffer plane j + R,
@@ -789,6 +803,7 @@ tile2d_step_kernel(const __grid_constant__ CUtensorMap map_p,    // p buffer, bo
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_sync();
     if (b1 <= b0) return;
     const int nload = b1 - b0;
 

@@ -1270,6 +1270,15 @@ static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStrea
             [&] { time_update_kernel<R, NDIM><<<grid, blk, 0, st>>>(p, s.D[0], s.D[1], s.D[2]); });
 }
 
+// Programmatic dependent launch of the tiled step kernels (fd_kernels.cuh
+// pdl_sync): single-slab contexts (the two-stream slab schedule orders its
+// launches through events), not while profiling (per-launch events);
+// FD_PDL=0 turns it off (A/B).
+static bool use_pdl(const fd_ctx *c) {
+    static const bool off = [] { const char *e = getenv("FD_PDL"); return e && e[0] == '0'; }();
+    return !off && !c->overlap && !c->opt_profile;
+}
+
 // In-kernel halo pushes of a boundary launch (FD_OPT_TRANSPORT = 1): buffer b1
 // (pnext) pushes `push1` planes per face, b2 (pnext2, two-step kernels) `push2`.
 static void set_push(const fd_ctx *c, const Slab &s, StepParams &p, int b1, int push1, int b2, int push2) {
@@ -1349,7 +1358,7 @@ static void launch_region(fd_ctx *c, Slab &s, Region &g, cudaStream_t st) {
     const bool push = c->opt_transport == 1 && g.boundary;
     if (push) set_push(c, s, p, c->iprev, c->opt_tsteps >= 2 ? c->H : c->R, -1, 0);
     const launch_fused_t go = t.launch[(c->d_gsp ? kVarSponge : 0) | (push ? kVarPeer : 0) | (c->kplane ? kVarKPlane : 0)];
-    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, mp, mpp, s.mK, p); });
+    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, mp, mpp, s.mK, p, use_pdl(c)); });
 }
 
 // Halo exchange of `depth` planes per face of field buffer b (b = -1: K).
@@ -1560,7 +1569,7 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     const bool push = c->opt_transport == 1 && g.boundary;
     if (push) set_push(c, s, p, f1, c->R, f2, c->H);
     const launch_fused_t go = t.launch[(c->d_gsp ? kVarSponge : 0) | (push ? kVarPeer : 0) | (c->kplane ? kVarKPlane : 0)];
-    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, m0, mm, s.mKe, p); });
+    tracked(c, FD_K_FUSED, st, [&] { go(grid, t.smem, st, m0, mm, s.mKe, p, use_pdl(c)); });
 }
 
 // S steps per launch (S = 2: tb2ws / tb2d; S >= 3: tbs2d, single slab).

@@ -18,7 +18,7 @@
 using namespace fdk;
 
 typedef void (*launch_fused_t)(dim3, int, cudaStream_t, const CUtensorMap &, const CUtensorMap &,
-                               const CUtensorMap &, const StepParams &);
+                               const CUtensorMap &, const StepParams &, bool pdl);
 
 constexpr int kVariants = 8;
 enum { kVarSponge = 1, kVarPeer = 2, kVarKPlane = 4 };
@@ -44,11 +44,23 @@ std::vector<TileCfg> tbs2d();         // tbs2d_step_kernel, 2D, S >= 3 (fd_tab_t
 }  // namespace fdtab
 
 #ifdef FD_TABLE_TU
+// pdl: launch with programmatic stream serialization (the kernels call
+// pdl_sync() after their prologue; fd_kernels.cuh)
 #define FD_LAUNCHER(NAME, KERNEL)                                                                            \
     template <class C, int V>                                                                                \
     static void NAME(dim3 grid, int smem, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,       \
-                     const CUtensorMap &c, const StepParams &p) {                                            \
-        KERNEL<C, (V & 1) != 0, (V & 2) != 0, (V & 4) != 0><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p);   \
+                     const CUtensorMap &c, const StepParams &p, bool pdl) {                                  \
+        if (!pdl) {                                                                                          \
+            KERNEL<C, (V & 1) != 0, (V & 2) != 0, (V & 4) != 0><<<grid, C::NTHREADS, smem, st>>>(a, b, c, p); \
+            return;                                                                                          \
+        }                                                                                                    \
+        cudaLaunchConfig_t cfg = {};                                                                         \
+        cudaLaunchAttribute at[1];                                                                           \
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                       \
+        at[0].val.programmaticStreamSerializationAllowed = 1;                                                \
+        cfg.gridDim = grid; cfg.blockDim = dim3(C::NTHREADS); cfg.dynamicSmemBytes = (size_t)smem;           \
+        cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;                                                   \
+        cudaLaunchKernelEx(&cfg, KERNEL<C, (V & 1) != 0, (V & 2) != 0, (V & 4) != 0>, a, b, c, p);           \
     }
 
 #define FD_VARIANT(T, C, KERNEL, LAUNCH, V)                                                                  \

@@ -164,6 +164,7 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_sync();
     if (z1e <= z0) return;
     // P^k load l: plane j = z0 - 2r + l (l < nload); aux load a (a = l - 2r >= 0):
     // plane z1 = z0 - r + a.  Stage A iteration a (l = a + 2r) computes P^{k+1}(z1);
@@ -599,6 +600,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_sync();
     if (v1 <= v0) return;
     const int nload = v1 - v0;
     // receiver i belongs to block v (receivers are sorted by (unit, v, z))

@@ -116,6 +116,7 @@ tbs2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, b
     // the ring slots' pads are read (never used) by the edge quads: keep them finite
     for (int i = tid; i < C::NRINGS * C::NR * C::RF; i += C::NTHREADS) sRing[i] = 0.f;
     __syncthreads();
+    pdl_sync();
     if (v1 <= v0) return;
     const int nload = v1 - v0;
     const int nx = (int)prm.nx;
