@@ -1271,12 +1271,14 @@ static void launch_unfused(const fd_ctx *c, fd_ctx *cm, const Slab &s, cudaStrea
 }
 
 // Programmatic dependent launch of the tiled step kernels (fd_kernels.cuh
-// pdl_sync): single-slab contexts (the two-stream slab schedule orders its
-// launches through events), not while profiling (per-launch events);
-// FD_PDL=0 turns it off (A/B).
+// pdl_sync): opt-in (FD_PDL=1), single-slab contexts (the two-stream slab
+// schedule orders its launches through events), not while profiling.  r2 A/B
+// (Gpts/s, PDL vs plain graph replay): C2 order 4 507.6 vs 500.8, order 2
+// 548.9 vs 560.9, C3 620.2 vs 618.8, orders 8 +-0.4 %: no consistent gain
+// over graph replay, whose launch gaps are already ~1 us.
 static bool use_pdl(const fd_ctx *c) {
-    static const bool off = [] { const char *e = getenv("FD_PDL"); return e && e[0] == '0'; }();
-    return !off && !c->overlap && !c->opt_profile;
+    static const bool on = [] { const char *e = getenv("FD_PDL"); return e && e[0] == '1'; }();
+    return on && !c->overlap && !c->opt_profile;
 }
 
 // In-kernel halo pushes of a boundary launch (FD_OPT_TRANSPORT = 1): buffer b1
