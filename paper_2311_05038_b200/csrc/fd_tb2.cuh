@@ -659,10 +659,6 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             }
             mbar_wait(&fullS[s], (l / C::NS) & 1);
             mbar_wait(&empty1[s1], ((l / C::N1) & 1) ^ 1);
-            // block-uniform: every point of this CTA's grown block is outside the
-            // band in x and z -- the band predicates need not be evaluated
-            const bool inner = !SP && x0 - 4 >= R && x0 + C::TX + 4 <= nx - R &&
-                               (int)prm.gz0 + rb - R >= R && (int)prm.gz0 + rb + C::TY + R <= (int)prm.nzg - R;
             const float *tp = sSt + s * C::STAGE, *tpm = tp + C::P0F, *tk = tpm + C::EF;
             float *t1 = sP1 + s1 * C::EF;
             float4 oraw[C::NYA];                                   // raw P^{k+1} (receivers)
@@ -689,17 +685,12 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                         float sx = __fmul_rn(c0, pc);
 #pragma unroll
                         for (int m = 1; m <= R; ++m) sx = __fmaf_rn(tap(R, m), __fadd_rn(av[4 + e - m], av[4 + e + m]), sx);
+                        float S = inx[e] ? sx : 0.f;
                         float szz = __fmul_rn(c0, pc);
 #pragma unroll
                         for (int m = 1; m <= R; ++m)
                             szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
-                        float S;
-                        if (inner) {
-                            S = __fadd_rn(sx, szz);            // = the band-rule form with both predicates true
-                        } else {
-                            S = inx[e] ? sx : 0.f;
-                            S = inz ? __fadd_rn(S, szz) : S;
-                        }
+                        S = inz ? __fadd_rn(S, szz) : S;
                         f4set(o, e, time_update<SP>(f4(k4, e), S, pc, f4(pm4, e), SP ? sponge_gz(prm, gz) : 1.f,
                                                     1.f, sgx[e]));
                     }
@@ -761,8 +752,6 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 if (act && prm.sx[s2] >= xb && prm.sx[s2] < xb + 4) smask |= 1u << s2;
         }
         mbar_wait(&full1[s1], (l / C::N1) & 1);
-        const bool inner = !SP && x0 >= R && x0 + C::TX <= nx - R &&
-                           (int)prm.gz0 + rb >= R && (int)prm.gz0 + rb + C::TY <= (int)prm.nzg - R;
         const float *tp = sSt + s * C::STAGE, *tk = tp + C::P0F + C::EF;
         const float *t1 = sP1 + s1 * C::EF;
         const int zt = rb + ri0;
@@ -788,17 +777,12 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                     float sx = __fmul_rn(c0, pc);
 #pragma unroll
                     for (int m = 1; m <= R; ++m) sx = __fmaf_rn(tap(R, m), __fadd_rn(av[4 + e - m], av[4 + e + m]), sx);
+                    float S = inx[e] ? sx : 0.f;
                     float szz = __fmul_rn(c0, pc);
 #pragma unroll
                     for (int m = 1; m <= R; ++m)
                         szz = __fmaf_rn(tap(R, m), __fadd_rn(f4(col[yy + R - m], e), f4(col[yy + R + m], e)), szz);
-                    float S;
-                    if (inner) {
-                        S = __fadd_rn(sx, szz);
-                    } else {
-                        S = inx[e] ? sx : 0.f;
-                        S = inz ? __fadd_rn(S, szz) : S;
-                    }
+                    S = inz ? __fadd_rn(S, szz) : S;
                     f4set(out[yy], e, time_update<SP>(f4(k4, e), S, pc, f4(pk4, e), sgz, 1.f, sgx[e]));
                 }
             }
