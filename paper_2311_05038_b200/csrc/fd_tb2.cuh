@@ -183,12 +183,12 @@ tb2ws_step_kernel(const __grid_constant__ CUtensorMap map_p0, const __grid_const
             tma_prefetch_desc(&map_p0); tma_prefetch_desc(&map_pm); tma_prefetch_desc(&map_k);
             for (int l = 0; l < nload; ++l) {
                 const int j = z0 - 2 * R + l, s = l % C::NSP;
-                mbar_wait(&emptyP[s], ((l / C::NSP) & 1) ^ 1);
+                mbar_wait_producer(&emptyP[s], ((l / C::NSP) & 1) ^ 1);
                 mbar_expect_tx(&fullP[s], C::P0_BYTES);
                 tma_load_3d(sP0 + s * C::P0F, &map_p0, &fullP[s], x0 - 8, y0 - 2 * R, j + halo_planes(R));
                 if (l >= 2 * R) {
                     const int a = l - 2 * R, z1 = j - R, sa = a % C::NSA;
-                    mbar_wait(&emptyA[sa], ((a / C::NSA) & 1) ^ 1);
+                    mbar_wait_producer(&emptyA[sa], ((a / C::NSA) & 1) ^ 1);
                     mbar_expect_tx(&fullA[sa], KZ ? C::AUX_BYTES / 2 : C::AUX_BYTES);
                     float *dst = sAux + sa * 2 * C::EF;
                     tma_load_3d(dst, &map_pm, &fullA[sa], x0 - 4, y0 - R, z1 + halo_planes(R));
@@ -617,7 +617,7 @@ tb2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
             for (int l = 0; l < nload; ++l) {
                 const int v = v0 + l, colu = v / nb;
                 const int s = l % C::NS, rb = prm.zlo + (v - colu * nb) * C::TY, x0 = colu * C::TX;
-                mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
+                mbar_wait_producer(&emptyS[s], ((l / C::NS) & 1) ^ 1);
                 mbar_expect_tx(&fullS[s], C::STAGE_BYTES - (KZ ? C::BXE * C::BYE * 4 : 0));
                 float *st = sSt + s * C::STAGE;
                 tma_load_3d(st, &map_p0, &fullS[s], x0 - 8, 0, rb - 2 * R + halo_planes(R));        // rows rb-2r.. (+r halo)

@@ -133,7 +133,7 @@ tbs2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, b
             for (int l = 0; l < nload; ++l) {
                 const int v = v0 + l, colu = v / nb;
                 const int s = l % C::NS, rb = prm.zlo + (v - colu * nb) * C::TY, x0 = colu * C::TX;
-                mbar_wait(&emptyS[s], ((l / C::NS) & 1) ^ 1);
+                mbar_wait_producer(&emptyS[s], ((l / C::NS) & 1) ^ 1);
                 mbar_expect_tx(&fullS[s], C::STAGE_BYTES);
                 float *st = sSt + s * C::STAGE;
                 // buffer row of local row z is z + 2r; the K halo buffer's is z + r

@@ -821,3 +821,37 @@ def test_traces_readback_into_preallocated_buffer(fd):
     assert T.shape == (33, 35) and np.array_equal(T, T2) and np.array_equal(T, T3)
     want = np.stack([[f[z, x] for f in fields] for z, x in recs])
     assert np.array_equal(T, want)
+
+
+def test_programmatic_dependent_launch_bitwise(fd, tmp_path):
+    """FD_PDL=1 (opt-in: the step kernels launched with programmatic stream
+    serialization, pdl_sync after their prologue) gives bitwise the results of
+    the default launches for every tiled kernel family: two-step 3D / 2D,
+    single-step 3D / 2D, three steps per launch; graphs on."""
+    import os
+    import subprocess
+    import sys
+    cases = [((40, 36, 140), 2, 0), ((35, 36, 130), 8, 0), ((300, 517), 2, 0), ((300, 517), 8, 0), ((300, 517), 2, 3)]
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys, numpy as np; sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[2])\n"
+            "import test_gpu_parity as t, paper_2311_05038_b200 as fd\n"
+            f"cases = {cases!r}\n"
+            "out = {}\n"
+            "for i, (dims, order, ts) in enumerate(cases):\n"
+            "    vel = t._rand_vel(dims, seed=101)\n"
+            "    src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0)]\n"
+            "    recs = [tuple(d // 3 for d in dims), tuple(d // 2 + 1 for d in dims)]\n"
+            "    r = t.run_gpu(fd, vel, 10.0, 5e-4, order, 53, src, recs, options={fd.FD_OPT_TSTEPS: ts})\n"
+            "    out[f'P{i}'], out[f'Pp{i}'], out[f'T{i}'] = r[0], r[1], r[2]\n"
+            "np.savez(sys.argv[3], **out)\n")
+    res = subprocess.run([sys.executable, "-c", code, os.path.dirname(here), here, str(tmp_path / "pdl.npz")],
+                         env={**os.environ, "FD_PDL": "1"}, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    got = np.load(tmp_path / "pdl.npz")
+    for i, (dims, order, ts) in enumerate(cases):
+        vel = _rand_vel(dims, seed=101)
+        src = [(tuple(d // 2 for d in dims), 25.0, 0.02, 1.0)]
+        recs = [tuple(d // 3 for d in dims), tuple(d // 2 + 1 for d in dims)]
+        ref = run_gpu(fd, vel, 10.0, 5e-4, order, 53, src, recs, options={fd.FD_OPT_TSTEPS: ts})
+        for k, a in zip("P Pp T".split(), ref[:3]):
+            assert np.array_equal(got[f"{k}{i}"], a), (i, k)
