@@ -222,6 +222,11 @@ fd_status fd_set_wavefield(fd_ctx *ctx, int which, const float *host_in);
  *                    16 B per grid-point update); bitwise equal
  *                    to single steps.  2D and 3D, orders 2-8; on z-slabs
  *                    (ranks, FD_OPT_VSLABS) 2r + r halo planes per two steps.
+ *                    3 or 4: S steps per launch on 2D single-slab contexts
+ *                    without the sponge frame, orders with (S-1) r <= 4
+ *                    (20 B per point per S updates); other
+ *                    contexts FD_ERR_STATE at the first fd_step.  Step counts
+ *                    that are not multiples of S end with single steps.
  *   FD_OPT_TB2TILE   index of the temporal-blocking tile configuration (-1 auto)
  *   FD_OPT_RESERVE   n >= 0: finish setup now -- allocate the step tables for n more
  *                    steps and capture the CUDA graphs the next fd_step calls will

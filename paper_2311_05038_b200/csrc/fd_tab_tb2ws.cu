@@ -38,5 +38,9 @@ std::vector<TileCfg> fdtab::tb2ws() {
         // r2: 3D r = 3, 4 (orders 6, 8), tuning-only (FD_OPT_TSTEPS=2): 64 x 16
         // tiles, stage A on the 72 x (16 + 2r) grown tile (1.6-1.7x the points)
         make_tb2ws<3, 64, 16, 2, 2, 1, 1, 1>(), make_tb2ws<4, 64, 16, 2, 2, 0, 0, 0>(),
-        make_tb2ws<4, 64, 16, 1, 2, 0, 0, 0>()};
+        make_tb2ws<4, 64, 16, 1, 2, 0, 0, 0>(),
+        // r2: 3D r = 2 on 128 x 16 tiles (stage A recomputes 1.33x instead of
+        // 1.41x): C3 order 4 415.7 vs 419 single-step, C4 428.4 vs 421.4 --
+        // a wash; order 4 keeps single steps by default
+        make_tb2ws<2, 128, 16, 2, 4, 2, 1, 1, 1>()};
 }
