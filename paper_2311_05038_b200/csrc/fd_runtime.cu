@@ -245,6 +245,7 @@ struct fd_ctx {
     int64_t gk0 = 0;
     // distributed
     ncclComm_t comm = nullptr;
+    bool nccl_self = false;               // FD_VSLAB_NCCL=1: virtual-slab halos through NCCL (1-rank comm)
     ncclUniqueId nccl_id;
     bool have_id = false;
     // kernel configuration
@@ -928,6 +929,25 @@ static fd_status build_kplane(fd_ctx *c) {
 static fd_status prepare(fd_ctx *c) {
     fd_status st = split_virtual(c, c->opt_vslabs);
     if (st) return st;
+    {
+        // test hook (FD_VSLAB_NCCL=1): virtual slabs exchange their halos with
+        // NCCL send/recv over a one-rank communicator (self peer) instead of
+        // device copies -- the NCCL calls, grouping and graph capture of the
+        // multi-rank exchange run on a single GPU (NCCL refuses two ranks on
+        // one device)
+        const char *e = getenv("FD_VSLAB_NCCL");
+        if (e && e[0] == '1' && c->slabs.size() > 1 && c->nranks == 1 && c->opt_transport == 0) {
+            if (!nccl().ok) return fail(FD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+            ncclUniqueId id;
+            ncclResult_t r = nccl().GetUniqueId(&id);
+            if (!r) r = nccl().CommInitRank(&c->comm, 1, id, 0);
+            if (r) {
+                c->poisoned = true;
+                return fail(FD_ERR_NCCL, "ncclCommInitRank (self): %s", nccl().GetErrorString(r));
+            }
+            c->nccl_self = true;
+        }
+    }
     if (!c->stream) {
         // no stream set: an own non-blocking stream (capturable for graphs)
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
@@ -1398,6 +1418,36 @@ static fd_status exchange(fd_ctx *c, std::initializer_list<XBuf> xs, cudaStream_
         }
         return FD_OK;
     }
+    if (c->nccl_self) {
+        // virtual slabs over NCCL (test hook): each halo is a send/recv pair to
+        // the own rank, issued in the same order so the pairs match
+        NcclApi &n = nccl();
+        ncclResult_t r = n.GroupStart();
+        for (size_t q = 0; q < c->slabs.size(); ++q) {
+            Slab &s = c->slabs[q];
+            for (const XBuf &x : xs) {
+                float *buf = base(s, x.b);
+                const int64_t H = hoff(x.b), d = x.depth;
+                const size_t cnt = (size_t)(d * pf);
+                if (q > 0) {
+                    Slab &l = c->slabs[q - 1];
+                    if (!r) r = n.Send(base(l, x.b) + (H + l.nz - d) * pf, cnt, kNcclFloat32, 0, c->comm, st);
+                    if (!r) r = n.Recv(buf + (H - d) * pf, cnt, kNcclFloat32, 0, c->comm, st);
+                }
+                if (q + 1 < c->slabs.size()) {
+                    Slab &u = c->slabs[q + 1];
+                    if (!r) r = n.Send(base(u, x.b) + H * pf, cnt, kNcclFloat32, 0, c->comm, st);
+                    if (!r) r = n.Recv(buf + (H + s.nz) * pf, cnt, kNcclFloat32, 0, c->comm, st);
+                }
+            }
+        }
+        ncclResult_t r2 = n.GroupEnd();
+        if (r || r2) {
+            c->poisoned = true;
+            return fail(FD_ERR_NCCL, "NCCL halo exchange (virtual slabs): %s", n.GetErrorString(r ? r : r2));
+        }
+        return FD_OK;
+    }
     for (size_t q = 0; q < c->slabs.size(); ++q) {
         Slab &s = c->slabs[q];
         for (const XBuf &x : xs) {
@@ -1642,7 +1692,7 @@ static bool graphs_usable(const fd_ctx *c) {
     // Every rank replays the same sequence (the graph choice depends on the
     // buffer roles and the step count only), so the captured sends and
     // receives pair up as the plain ones do.
-    const bool ranks_ok = c->nranks == 1 || (c->opt_transport == 0 && c->comm && c->injected && c->k > 0);
+    const bool ranks_ok = (c->nranks == 1 && !c->comm) || (c->opt_transport == 0 && c->comm && c->injected && c->k > 0);
     return c->opt_graph && ranks_ok && !c->opt_profile && c->d_k && c->stream && !c->resident;
 }
 

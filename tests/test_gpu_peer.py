@@ -170,3 +170,49 @@ def test_nccl_init_failure_poisons_the_context(fd, tmp_path):
     out = res.stdout
     assert f"STEP {fd.FD_ERR_NCCL}" in out, out + res.stderr[-2000:]
     assert f"AGAIN {fd.FD_ERR_STATE}" in out and "DESTROYED" in out, out
+
+
+def test_virtual_slabs_over_nccl_bitwise(fd, oracle, tmp_path):
+    """The NCCL send/recv exchange on one GPU: with FD_VSLAB_NCCL=1 virtual
+    slabs move their halos with ncclSend/ncclRecv pairs over a one-rank
+    communicator (self peer) in one group per exchange -- the NCCL calls of
+    the multi-rank path, on the comm stream of the overlapped schedule and
+    captured into the CUDA graphs.  Bitwise equal to one slab; the oracle
+    within 1e-4; the communicator is live (fd_get_info comm_nranks == 1)."""
+    cases = [((40, 30, 70), 2, 2, 2), ((45, 26, 50), 8, 3, 1), ((96, 300), 4, 3, 2), ((70, 140), 8, 2, 1),
+             ((60, 29, 66), 2, 3, 1)]
+    code = ("import sys, numpy as np; sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[2])\n"
+            "import test_gpu_parity as t, paper_2311_05038_b200 as fd\n"
+            f"cases = {cases!r}\n"
+            "out = {}\n"
+            "for i, (dims, order, ns, ts) in enumerate(cases):\n"
+            "    vel = t._rand_vel(dims, seed=73)\n"
+            "    nz = dims[0]; rest = tuple(d // 2 for d in dims[1:])\n"
+            "    src = [((nz // 2,) + rest, 25.0, 0.02, 1.0), ((nz // 3,) + rest, 15.0, 0.03, -0.4)]\n"
+            "    recs = [(nz // 2 - 1,) + rest, (nz // 3 + 1,) + rest, (nz - 3,) + rest]\n"
+            "    for g in (1, 0):\n"
+            "        r = t.run_gpu(fd, vel, 10.0, 5e-4, order, 37, src, recs,\n"
+            "                      options={fd.FD_OPT_VSLABS: ns, fd.FD_OPT_TSTEPS: ts, fd.FD_OPT_GRAPH: g})\n"
+            "        out[f'P{i}_{g}'], out[f'Pp{i}_{g}'], out[f'T{i}_{g}'] = r[0], r[1], r[2]\n"
+            "        out[f'c{i}_{g}'] = r[3]['comm_nranks']; out[f'gs{i}_{g}'] = r[3]['graph_steps']\n"
+            "np.savez(sys.argv[3], **out)\n")
+    here = os.path.dirname(os.path.abspath(__file__))
+    res = subprocess.run([sys.executable, "-c", code, ROOT, here, str(tmp_path / "vn.npz")],
+                         env={**os.environ, "FD_VSLAB_NCCL": "1", "NCCL_DEBUG": "WARN"}, capture_output=True,
+                         text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
+    got = np.load(tmp_path / "vn.npz")
+    for i, (dims, order, ns, ts) in enumerate(cases):
+        vel = _rand_vel(dims, seed=73)
+        nz = dims[0]
+        rest = tuple(d // 2 for d in dims[1:])
+        src = [((nz // 2,) + rest, 25.0, 0.02, 1.0), ((nz // 3,) + rest, 15.0, 0.03, -0.4)]
+        recs = [(nz // 2 - 1,) + rest, (nz // 3 + 1,) + rest, (nz - 3,) + rest]
+        ref = run_gpu(fd, vel, 10.0, 5e-4, order, 37, src, recs, options={fd.FD_OPT_TSTEPS: 1})
+        for g in (1, 0):
+            assert int(got[f"c{i}_{g}"]) == 1, (i, g)
+            assert (int(got[f"gs{i}_{g}"]) > 0) == (g == 1), (i, g)
+            for k, a in zip("P Pp T".split(), ref[:3]):
+                assert np.array_equal(got[f"{k}{i}_{g}"], a), (i, g, k)
+        Po, _, To = oracle.run(vel, 10.0, 5e-4, order, 37, src, recs, nthreads=4)
+        assert rel_l2(ref[0], Po) <= TOL and rel_l2(ref[2], To) <= TOL
