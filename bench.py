@@ -605,6 +605,7 @@ def _emit(args, wl, world, rank, gpts, ms_step, info, launches, clk, finite, e2e
             "algorithmic_bytes_per_launch": bytes_per_launch, "steps_per_launch": steps_per_launch,
             "points_per_launch": npts_local,
             "kernel": "resident_kernel" if resident else
+                      "rs2d_step_kernel" if int(info.get("tb_kind", 0)) == 1 else
                       {(3, 1): "fused_step_kernel", (3, 2): "tb2ws_step_kernel", (2, 1): "tile2d_step_kernel",
                        (2, 2): "tb2d_step_kernel", (2, 3): "tbs2d_step_kernel",
                        (2, 4): "tbs2d_step_kernel"}[(wl.ndim, steps_per_launch)],

@@ -291,6 +291,8 @@ typedef struct {
     int kplane;                /* 1 when the kernels read K per plane (FD_OPT_KPLANE)    */
     int comm_nranks;           /* ranks of the NCCL communicator (ncclCommCount; 0: none) */
     int64_t graph_steps;       /* steps advanced by CUDA-graph replay so far             */
+    int tb_kind;               /* multi-step kernel family: 0 TMA-staged tiles (tb2ws,
+                                  tb2d, tbs2d), 1 register-streamed 2D strips (rs2d)    */
 } fd_info;
 fd_status fd_get_info(fd_ctx *ctx, fd_info *out);
 

@@ -105,7 +105,8 @@ struct StepParams {
     int32_t lin;            // tb2d linear mode: units sharing the ntx * nb blocks (0: chunked)
     float *pnext;           // base of the p_prev buffer (overwritten in place); TB2: the C buffer
     float *pnext2;          // TB2 only: the D buffer (P^{k+2})
-    const float *p;         // base of the p buffer (naive kernel only)
+    const float *p;         // base of the p buffer (naive kernel, register-streamed 2D kernel)
+    const float *pm;        // base of the p_prev buffer (register-streamed 2D kernel)
     const float *K;         // K base (naive kernel only)
     // step index: k, or *kdev + koff when replayed from a CUDA graph
     int64_t k;
@@ -125,6 +126,8 @@ struct StepParams {
     const float *gsp;       // sponge frame (R#18): g_x[nx], g_y[ny], g_z[nzg] (global z); null = off
     const float *kz;        // FD_OPT_KPLANE: K of local plane z at kz[z] (z in [-r, nz + r)); the KZ
                             // kernel variants read it instead of the K field
+    unsigned long long *ws; // rs2d work stealing: one word per warp of the launch (null: static split)
+    int32_t nws;            // words (warps) in ws
 };
 
 // Per-plane K (FD_OPT_KPLANE): when K depends on the

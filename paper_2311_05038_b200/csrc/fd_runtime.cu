@@ -116,7 +116,7 @@ static const std::vector<TileCfg> &tile_table() {
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = [] {
         std::vector<TileCfg> v;
-        for (auto part : {fdtab::tb2ws, fdtab::tb2d, fdtab::tbs2d}) {
+        for (auto part : {fdtab::tb2ws, fdtab::tb2d, fdtab::rs2d, fdtab::tbs2d}) {
             auto p = part();
             v.insert(v.end(), p.begin(), p.end());
         }
@@ -189,6 +189,8 @@ struct Region {
     int ctas = 0;
     bool boundary = false;      // launched on the comm stream before the exchange
     int32_t *d_rec = nullptr;   // [4 * nrec + units + 1]: z, y, x, id, CSR offsets
+    unsigned long long *d_ws = nullptr;   // rs2d work-stealing words, one per warp (fd_rs2d.cuh)
+    int nws = 0;
     int nrec = 0;
 };
 
@@ -331,7 +333,7 @@ static void free_slab(Slab &s) {
     dev_free(s.Kh); dev_free(s.d_src_raw); dev_free(s.kzt);
     s.Kh = s.K = s.d_src_raw = s.kzt = nullptr;
     for (auto &r : s.regions) { dev_free(r.d_rec); r.d_rec = nullptr; }
-    for (auto &r : s.tb2) { dev_free(r.d_rec); r.d_rec = nullptr; }
+    for (auto &r : s.tb2) { dev_free(r.d_rec); r.d_rec = nullptr; dev_free(r.d_ws); r.d_ws = nullptr; }
 }
 
 static void drop_graphs(fd_ctx *c) {
@@ -592,6 +594,7 @@ static int64_t ntiles_of(const fd_ctx *c, const TileCfg &t) {
 // whose CTAs are short), then pick among nearby counts the best
 // fill x (chunk / (chunk + warm-up planes)).
 static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
+    if (t.kind == 1) return 1;   // rs2d: one receiver list per column strip, persistent grid (rs2d_ctas)
     if (c->opt_zchunks > 0) return (int)std::min<int64_t>(c->opt_zchunks, std::max<int64_t>(1, span));
     const int64_t slots = (int64_t)c->nsm * std::max(occ, 1), ntiles = ntiles_of(c, t);
     // 3D: chunks of >= max(4r, 8) planes (the 2r warm-up planes stay small);
@@ -626,6 +629,17 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
     return (int)best;
 }
 
+// rs2d (register-streamed 2D strips): a persistent grid -- one wave of resident
+// CTAs, fewer when the region has under 16 rows per warp -- whose warps cut
+// the column strips into pieces and balance by work stealing (fd_rs2d.cuh).
+// FD_OPT_ZCHUNKS pins the CTA count (tests: a few warps, many pieces each).
+static int rs2d_ctas(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
+    if (c->opt_zchunks > 0) return (int)std::min<int64_t>(c->opt_zchunks, (int64_t)c->nsm * std::max(occ, 1));
+    const int64_t ntx = (c->nxg + t.tx - 1) / t.tx;
+    const int64_t want = (ntx * span + (int64_t)t.ny * 16 - 1) / ((int64_t)t.ny * 16);
+    return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->nsm * std::max(occ, 1), want));
+}
+
 // 2D two-step launches (tb2d) can split the region's ntx * nb row blocks into
 // one wave of equal contiguous ranges ("linear" units that cross column
 // boundaries): one pipeline warm-up per CTA and no wave tail, vs the chunked
@@ -638,7 +652,7 @@ static int chunks_for(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) 
 static int lin_units(const fd_ctx *c, const TileCfg &t, int occ, int64_t span) {
     const bool tb2d = c->ndim == 2 && c->tb2 >= 0 && &t == &tb2_table()[c->tb2];
     static const bool on = [] { const char *e = getenv("FD_TB2D_LINEAR"); return e && e[0] == '1'; }();
-    if (!tb2d || c->opt_zchunks > 0 || !on) return 0;
+    if (!tb2d || t.kind != 0 || c->opt_zchunks > 0 || !on) return 0;
     const int64_t nb = (span + t.ty - 1) / t.ty, V = ((c->nxg + t.tx - 1) / t.tx) * nb;
     return (int)std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)c->nsm * std::max(occ, 1)));
 }
@@ -758,6 +772,18 @@ static fd_status upload_region_receivers(fd_ctx *c, const Slab &s, Region &g, co
     g.d_rec = (int32_t *)dev_alloc(h.size() * 4);
     if (!g.d_rec) return fail(FD_ERR_NOMEM, "receiver table allocation failed");
     CUDA_TRY(c, cudaMemcpy(g.d_rec, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    // rs2d work stealing: one 64-bit word per warp (rows < 2^20, units < 2^14;
+    // FD_RS_STEAL=0: static split)
+    dev_free(g.d_ws);
+    g.d_ws = nullptr;
+    g.nws = 0;
+    static const bool steal = [] { const char *e = getenv("FD_RS_STEAL"); return !(e && e[0] == '0'); }();
+    if (t && t->kind == 1 && g.lin == 0 && steal && span < (1 << 20) - 4096 && nunits < (1 << 14)) {
+        g.nws = rs2d_ctas(c, *t, c->tb2occ, span) * t->ny;
+        g.d_ws = (unsigned long long *)dev_alloc((size_t)g.nws * 8);
+        if (!g.d_ws) return fail(FD_ERR_NOMEM, "work-stealing array allocation failed");
+        CUDA_TRY(c, cudaMemset(g.d_ws, 0, (size_t)g.nws * 8));
+    }
     return FD_OK;
 }
 
@@ -1009,6 +1035,12 @@ static fd_status prepare(fd_ctx *c) {
         // unless a single-step tile is pinned
         const bool tb_wins = c->ndim == 3 ? c->R == 1 : c->R <= 2;
         c->opt_tsteps = (tb_wins && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
+        // 2D order 2 on one slab with the band rule: three steps per pass in
+        // the register-streamed kernel (r3, C2: 681 Gpts/s vs 562 for the
+        // two-step tb2d kernel)
+        if (c->opt_tsteps == 2 && c->ndim == 2 && c->R == 1 && c->nranks == 1 && c->slabs.size() == 1 &&
+            c->sponge_nb == 0 && c->opt_transport == 0 && c->opt_tb2tile < 0)
+            c->opt_tsteps = 3;
     }
     const bool multi = c->nranks > 1 || c->slabs.size() > 1;
     // overlapped schedule (boundary planes + exchange on the comm stream,
@@ -1610,12 +1642,16 @@ static void launch_tb2(fd_ctx *c, Slab &s, Region &g, int f1, int f2, cudaStream
     StepParams p;
     fill_params(c, s, &g, p, c->k);
     p.p = cur_buf(c, s);
+    p.pm = prev_buf(c, s);
     p.pnext = s.F[f1];
     p.pnext2 = s.F[f2];
     p.K = s.K;
     p.ntx = (int32_t)((c->nxg + t.tx - 1) / t.tx);
     p.nty = (int32_t)((c->nyg + t.ty - 1) / t.ty);
-    const dim3 grid((unsigned)(p.lin > 0 ? p.lin : p.ntx * p.nty * p.nchunks));
+    p.ws = g.d_ws;
+    p.nws = g.nws;
+    const dim3 grid((unsigned)(t.kind == 1 ? rs2d_ctas(c, t, c->tb2occ, g.zhi - g.zlo)
+                                           : p.lin > 0 ? p.lin : p.ntx * p.nty * p.nchunks));
     g.ctas = (int)grid.x;
     const CUtensorMap &m0 = s.mP0[c->icur], &mm = s.mPm[c->iprev];
     const bool push = c->opt_transport == 1 && g.boundary;
@@ -1895,6 +1931,15 @@ fd_status fd_step(fd_ctx *c, int64_t n) {
         s = resident_steps(c, n);
         if (s) return s;
         i = n;
+    }
+    if (c->comm && c->opt_transport == 0 && c->k == 0 && c->opt_graph && !c->opt_profile && !c->resident &&
+        n - i > graph_len(c)) {
+        // NCCL exchanges are captured only after a first plain pass (NCCL's
+        // lazy connection setup must happen outside any capture)
+        const int S = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].steps : 1;
+        s = advance_plain(c, S);
+        if (s) return s;
+        i += S;
     }
     if (graphs_usable(c) && n - i >= graph_len(c)) {
         // replay G-step graphs; the device counter d_k carries k
@@ -2289,6 +2334,7 @@ fd_status fd_get_info(fd_ctx *c, fd_info *o) {
     o->order = c->order;
     o->device_bytes = c->dev_bytes;
     o->steps_per_launch = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].steps : 1;
+    o->tb_kind = (c->opt_tsteps >= 2 && c->tb2 >= 0) ? tb2_table()[c->tb2].kind : 0;
     o->kplane = c->kplane ? 1 : 0;
     o->graph_steps = c->graph_steps;
     if (c->comm && nccl().CommCount) {

@@ -30,7 +30,9 @@ struct TileCfg {
     int threads, smem;
     const void *kernel[kVariants];
     launch_fused_t launch[kVariants];
-    int steps = 2;       // time steps per launch (temporal-blocking table: 2, or S of tbs2d)
+    int steps = 2;       // time steps per launch (temporal-blocking table: 2, or S of tbs2d / rs2d)
+    int kind = 0;        // 0: TMA-staged tiles; 1: register-streamed 2D strips (rs2d_step_kernel, no
+                         // shared memory; tx = own columns per strip, ty = 1, ny = warps per CTA)
     bool full() const { return kernel[kVariants - 1] != nullptr; }
 };
 
@@ -41,6 +43,7 @@ std::vector<TileCfg> tiles2d();       // tile2d_step_kernel           (fd_tab_2d
 std::vector<TileCfg> tb2ws();         // tb2ws_step_kernel, 3D r <= 2  (fd_tab_tb2ws.cu)
 std::vector<TileCfg> tb2d();          // tb2d_step_kernel, 2D          (fd_tab_tb2d.cu)
 std::vector<TileCfg> tbs2d();         // tbs2d_step_kernel, 2D, S >= 3 (fd_tab_tbs.cu)
+std::vector<TileCfg> rs2d();          // rs2d_step_kernel, 2D, S >= 2  (fd_tab_rs2d.cu)
 }  // namespace fdtab
 
 #ifdef FD_TABLE_TU

@@ -61,7 +61,7 @@ class FdInfo(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int), ("zchunks", ctypes.c_int), ("order", ctypes.c_int),
                 ("device_bytes", ctypes.c_double), ("steps_per_launch", ctypes.c_int),
                 ("cluster_ctas", ctypes.c_int), ("kplane", ctypes.c_int), ("comm_nranks", ctypes.c_int),
-                ("graph_steps", ctypes.c_int64)]
+                ("graph_steps", ctypes.c_int64), ("tb_kind", ctypes.c_int)]
 
     def as_dict(self) -> dict:
         d = {}
