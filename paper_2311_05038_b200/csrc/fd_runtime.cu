@@ -1035,12 +1035,12 @@ static fd_status prepare(fd_ctx *c) {
         // unless a single-step tile is pinned
         const bool tb_wins = c->ndim == 3 ? c->R == 1 : c->R <= 2;
         c->opt_tsteps = (tb_wins && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
-        // 2D order 2 on one slab with the band rule: three steps per pass in
-        // the register-streamed kernel (r3, C2: 681 Gpts/s vs 562 for the
-        // two-step tb2d kernel)
-        if (c->opt_tsteps == 2 && c->ndim == 2 && c->R == 1 && c->nranks == 1 && c->slabs.size() == 1 &&
+        // 2D orders 2 / 4 on one slab with the band rule: four / three steps
+        // per pass in the register-streamed kernel (r3, C2: 723 / 622 Gpts/s
+        // vs 562 / 500 for the two-step tb2d kernel)
+        if (c->opt_tsteps == 2 && c->ndim == 2 && c->R <= 2 && c->nranks == 1 && c->slabs.size() == 1 &&
             c->sponge_nb == 0 && c->opt_transport == 0 && c->opt_tb2tile < 0)
-            c->opt_tsteps = 3;
+            c->opt_tsteps = c->R == 1 ? 4 : 3;
     }
     const bool multi = c->nranks > 1 || c->slabs.size() > 1;
     // overlapped schedule (boundary planes + exchange on the comm stream,

@@ -20,13 +20,16 @@ static TileCfg make_rs2d() {
 
 std::vector<TileCfg> fdtab::rs2d() {
     return {
-        // three / four steps per pass (single slab, band rule): the 2D order-2
-        // default is the first S = 3 entry (r3, C2: cp.async rows 681 Gpts/s,
-        // TMA rows 651; 4 warps per CTA, 16 rows in flight per warp, 2 CTAs per SM)
-        make_rs2d<1, 3, 1, 4, 16, 2, false, false>(), make_rs2d<1, 3, 1, 4, 16, 2>(),
-        make_rs2d<1, 4, 1, 4, 16, 2, false, false>(), make_rs2d<1, 4, 1, 4, 16, 2>(),
-        make_rs2d<2, 3, 2, 4, 16, 2, false, false>(), make_rs2d<2, 3, 2, 4, 16, 2>(),
-        make_rs2d<2, 4, 2, 4, 16, 2>(),
+        // three / four steps per pass (single slab, band rule, K field or
+        // per-plane K): the 2D defaults are the first entry of each (r, S) --
+        // r3 on C2 with work stealing: order 2 S = 4 723 Gpts/s (S = 3 681),
+        // order 4 S = 3 622 (two-step tb2d: 562 / 500); cp.async rows beat TMA
+        // rows here (S = 4: 723 vs 629); 4 warps per CTA, 16 rows in flight
+        // per warp, 2 CTAs per SM
+        make_rs2d<1, 4, 1, 4, 16, 2, true, false>(), make_rs2d<1, 4, 1, 4, 16, 2>(),
+        make_rs2d<1, 3, 1, 4, 16, 2, true, false>(), make_rs2d<1, 3, 1, 4, 16, 2>(),
+        make_rs2d<2, 3, 2, 4, 16, 2, true, false>(), make_rs2d<2, 3, 2, 4, 16, 2>(),
+        make_rs2d<2, 4, 2, 4, 16, 2, false, false>(),
         // two steps per pass (tuning-only behind tb2d: C2 order 2 478 vs 562)
         make_rs2d<1, 2, 1, 4, 16, 2, true>(), make_rs2d<1, 2, 1, 4, 16, 2, false, false>(),
         make_rs2d<2, 2, 1, 4, 16, 2, true>(),

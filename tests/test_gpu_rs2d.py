@@ -128,19 +128,20 @@ def test_rs2d_virtual_slabs_and_sponge(fd, oracle, order):
                     assert np.array_equal(a, b), (tile, ns, sponge)
 
 
-def test_rs2d_is_the_2d_order2_default(fd):
-    """Auto policy: 2D order 2 on one slab with the band rule runs three steps
-    per pass in the register-streamed kernel; slabs and the sponge frame keep
-    two steps per pass."""
+@pytest.mark.parametrize("order,S", [(2, 4), (4, 3)])
+def test_rs2d_is_the_2d_default(fd, order, S):
+    """Auto policy: 2D orders 2 / 4 on one slab with the band rule run four /
+    three steps per pass in the register-streamed kernel; slabs and the
+    sponge frame keep two steps per pass."""
     vel = _rand_vel((300, 700), seed=3)
-    with fd.Simulation(vel, 10.0, 5e-4, 2, options=tiled(fd)) as sim:
+    with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd)) as sim:
         sim.step(8)
         info = sim.info()
-    assert info["tb_kind"] == 1 and info["steps_per_launch"] == 3, info
-    with fd.Simulation(vel, 10.0, 5e-4, 2, options=tiled(fd, {fd.FD_OPT_VSLABS: 2})) as sim:
+    assert info["tb_kind"] == 1 and info["steps_per_launch"] == S, info
+    with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd, {fd.FD_OPT_VSLABS: 2})) as sim:
         sim.step(8)
         assert sim.info()["steps_per_launch"] == 2
-    with fd.Simulation(vel, 10.0, 5e-4, 2, options=tiled(fd)) as sim:
+    with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd)) as sim:
         sim.set_sponge(10, 0.02)
         sim.step(8)
         assert sim.info()["steps_per_launch"] == 2
