@@ -77,7 +77,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // the value of register o.e of the owning lane (lane = (x - xq0) / 4) moved by
 // shuffle.  Advances rp; returns the next receiver's row (or 0x7fffffff past
 // zb).  Warp-uniform call.
-__device__ __noinline__ int rs_record(float4 o, int z, int zb, int &rp, int rend, int xq0, const Receivers &rec,
+static __device__ __noinline__ int rs_record(float4 o, int z, int zb, int &rp, int rend, int xq0, const Receivers &rec,
                                       float *trow) {
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -128,7 +128,7 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t *z, int rp, int re
 }
 // Eager injection of w at the sources of this lane's quad on row z, in
 // registration order; `raw`: also store the pre-injection value (src_raw).
-__device__ __noinline__ float4 rs_inject(float4 o, int z, uint32_t smask, int xb, bool raw, const StepParams &prm,
+static __device__ __noinline__ float4 rs_inject(float4 o, int z, uint32_t smask, int xb, bool raw, const StepParams &prm,
                                          const float *wv) {
     for (int s2 = 0; s2 < prm.nsrc; ++s2) {
         if (!((smask >> s2) & 1u) || prm.sz[s2] != z) continue;

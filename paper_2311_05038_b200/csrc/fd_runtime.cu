@@ -116,7 +116,7 @@ static const std::vector<TileCfg> &tile_table() {
 static const std::vector<TileCfg> &tb2_table() {
     static const std::vector<TileCfg> t = [] {
         std::vector<TileCfg> v;
-        for (auto part : {fdtab::tb2ws, fdtab::tb2d, fdtab::rs2d, fdtab::tbs2d}) {
+        for (auto part : {fdtab::tb2ws, fdtab::tb2d, fdtab::rs2d, fdtab::rs2d_x, fdtab::tbs2d}) {
             auto p = part();
             v.insert(v.end(), p.begin(), p.end());
         }
@@ -1035,11 +1035,12 @@ static fd_status prepare(fd_ctx *c) {
         // unless a single-step tile is pinned
         const bool tb_wins = c->ndim == 3 ? c->R == 1 : c->R <= 2;
         c->opt_tsteps = (tb_wins && c->opt_kernel == 0 && c->opt_tile < 0) ? 2 : 1;
-        // 2D orders 2 / 4 on one slab with the band rule: four / three steps
-        // per pass in the register-streamed kernel (r3, C2: 723 / 622 Gpts/s
-        // vs 562 / 500 for the two-step tb2d kernel)
-        if (c->opt_tsteps == 2 && c->ndim == 2 && c->R <= 2 && c->nranks == 1 && c->slabs.size() == 1 &&
-            c->sponge_nb == 0 && c->opt_transport == 0 && c->opt_tb2tile < 0)
+        // 2D orders 2 / 4 / 6 on one slab with the band rule: four / three /
+        // three steps per pass in the register-streamed kernel (r3, C2: 723 /
+        // 622 / 441 Gpts/s vs 562 / 500 two-step tb2d and 390 single-step;
+        // DESIGN.md section 5.12); order 8 stays on single steps (319 vs 385)
+        if (c->ndim == 2 && c->R <= 3 && c->opt_kernel == 0 && c->opt_tile < 0 && c->nranks == 1 &&
+            c->slabs.size() == 1 && c->sponge_nb == 0 && c->opt_transport == 0 && c->opt_tb2tile < 0)
             c->opt_tsteps = c->R == 1 ? 4 : 3;
     }
     const bool multi = c->nranks > 1 || c->slabs.size() > 1;
@@ -1164,7 +1165,7 @@ static fd_status prepare(fd_ctx *c) {
     // per-plane K once K and its halos are final (peer-transport ranks receive
     // K's halos with the first exchange: they keep the K field)
     const bool kz_compiled = c->tile >= 0 && tile_table()[c->tile].full() &&
-                             (c->opt_tsteps < 2 || (c->tb2 >= 0 && tb2_table()[c->tb2].full()));
+                             (c->opt_tsteps < 2 || (c->tb2 >= 0 && tb2_table()[c->tb2].kernel[kVarKPlane]));
     if (c->opt_kplane && c->opt_kernel == 0 && !c->resident && !(c->nranks > 1 && c->opt_transport == 1) &&
         kz_compiled) {
         st = build_kplane(c);

@@ -43,7 +43,8 @@ std::vector<TileCfg> tiles2d();       // tile2d_step_kernel           (fd_tab_2d
 std::vector<TileCfg> tb2ws();         // tb2ws_step_kernel, 3D r <= 2  (fd_tab_tb2ws.cu)
 std::vector<TileCfg> tb2d();          // tb2d_step_kernel, 2D          (fd_tab_tb2d.cu)
 std::vector<TileCfg> tbs2d();         // tbs2d_step_kernel, 2D, S >= 3 (fd_tab_tbs.cu)
-std::vector<TileCfg> rs2d();          // rs2d_step_kernel, 2D, S >= 2  (fd_tab_rs2d.cu)
+std::vector<TileCfg> rs2d();          // rs2d_step_kernel, 2D, defaults (fd_tab_rs2d.cu)
+std::vector<TileCfg> rs2d_x();        // rs2d_step_kernel, 2D, tuning   (fd_tab_rs2d_x.cu)
 }  // namespace fdtab
 
 #ifdef FD_TABLE_TU

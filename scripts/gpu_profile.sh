@@ -19,7 +19,7 @@ for spec in $SPECS; do
       python bench.py --config $cfg --order $ord --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --reps 1 --tsteps $ts $kzf \
       > /dev/null 2>&1
   # full capture of one steady-state launch of the step kernel
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-step_kernel} -s ${KSKIP:-5} -c 1 \
       -o gpurun_out/prof_${TAG}_${cfg}_o${ord}${sfx} -f \
       python bench.py --config $cfg --order $ord --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --reps 1 --tsteps $ts $kzf \
       > /dev/null 2>&1

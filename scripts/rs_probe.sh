@@ -9,7 +9,7 @@ T=$(mktemp -d)
   echo '#include "fd_rs2d.cuh"'
   echo '#include "fd_tables.cuh"'
   echo 'FD_LAUNCHER(launch_rs2d, rs2d_step_kernel)'
-  echo 'template <int R, int S, int HQ, int W, int Q, int MINB = 1, bool TMA = true>'
+  echo 'template <int R, int S, int HQ, int W, int Q, int MINB = 1, bool TMA = false>'
   echo 'static TileCfg make_rs2d() { using C = CfgRS2<R, S, HQ, W, Q, MINB, TMA>;'
   echo '  TileCfg t{2, R, C::TX, 1, W, Q, C::U, 64, 64, 8, 8, C::NTHREADS, C::SMEM_BYTES, {}, {}};'
   echo "  FD_VARIANT(t, C, rs2d_step_kernel, launch_rs2d, ${VARIANT:-0}); return t; }"

@@ -63,7 +63,7 @@ def _gpu_run(fd, wl, vel):
         return sim.wavefield(), sim.wavefield(fd.FD_FIELD_PREV), sim.traces(), sim.info()
 
 
-@pytest.mark.parametrize("name,order", [("C1", 2), ("C1", 8), ("C2", 2), ("C2", 8), ("C3", 2), ("C3", 8)])
+@pytest.mark.parametrize("name,order", [("C1", 2), ("C1", 8), ("C2", 2), ("C2", 4), ("C2", 6), ("C2", 8), ("C3", 2), ("C3", 8)])
 def test_full_length_parity(fd, oracle, name, order):
     from workloads import config
     wl = config(name, order=order)

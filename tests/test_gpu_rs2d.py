@@ -60,7 +60,7 @@ def _events(dims, order):
     return src, recs
 
 
-@pytest.mark.parametrize("dims,order,S", [((150, 517), 2, 2), ((131, 250), 4, 2), ((97, 361), 6, 2),
+@pytest.mark.parametrize("dims,order,S", [((150, 517), 2, 2), ((131, 250), 4, 2), ((97, 361), 6, 2), ((103, 330), 6, 3),
                                           ((90, 245), 8, 2), ((123, 517), 2, 3), ((101, 300), 2, 4),
                                           ((117, 400), 4, 3), ((90, 250), 4, 4), ((70, 90), 2, 2),
                                           ((64, 100), 4, 4)])
@@ -128,11 +128,11 @@ def test_rs2d_virtual_slabs_and_sponge(fd, oracle, order):
                     assert np.array_equal(a, b), (tile, ns, sponge)
 
 
-@pytest.mark.parametrize("order,S", [(2, 4), (4, 3)])
+@pytest.mark.parametrize("order,S", [(2, 4), (4, 3), (6, 3)])
 def test_rs2d_is_the_2d_default(fd, order, S):
-    """Auto policy: 2D orders 2 / 4 on one slab with the band rule run four /
-    three steps per pass in the register-streamed kernel; slabs and the
-    sponge frame keep two steps per pass."""
+    """Auto policy: 2D orders 2 / 4 / 6 on one slab with the band rule run four /
+    three / three steps per pass in the register-streamed kernel; slabs and
+    the sponge frame keep two steps per pass (order 6: single steps)."""
     vel = _rand_vel((300, 700), seed=3)
     with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd)) as sim:
         sim.step(8)
@@ -140,8 +140,8 @@ def test_rs2d_is_the_2d_default(fd, order, S):
     assert info["tb_kind"] == 1 and info["steps_per_launch"] == S, info
     with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd, {fd.FD_OPT_VSLABS: 2})) as sim:
         sim.step(8)
-        assert sim.info()["steps_per_launch"] == 2
+        assert sim.info()["steps_per_launch"] == (2 if order <= 4 else 1)
     with fd.Simulation(vel, 10.0, 5e-4, order, options=tiled(fd)) as sim:
         sim.set_sponge(10, 0.02)
         sim.step(8)
-        assert sim.info()["steps_per_launch"] == 2
+        assert sim.info()["steps_per_launch"] == (2 if order <= 4 else 1)
