@@ -11,8 +11,9 @@ z-chunks), virtual slabs with the overlapped schedule, CUDA-graph replay, the
 naive and unfused reference paths, the two-steps-per-launch kernels
 (3D and 2D, one slab and virtual slabs), the peer-push and sponge variants,
 the per-plane-K (KZ) variants and the cluster-resident kernel.  With
-FD_TB2D_LINEAR=1 the 2D two-step launches use linear units (r2).  r3: every
-register-streamed 2D configuration (rs2d, S = 2..4), with its work stealing.
+FD_TB2D_LINEAR=1 the 2D two-step launches use linear units (r2).  r3: the
+register-streamed 2D defaults (rs2d, S = 3, 4; the 2D single-slab default
+policy), with few warps (long runs, work stealing).
 """
 import os
 import sys
@@ -21,24 +22,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-
-
-def rs2d_tiles(fd, order):
-    """(S, index) of the rs2d entries of the temporal-blocking table for `order`."""
-    from paper_2311_05038_b200 import fd as fdm
-    vel = np.full((40, 64), 2000.0, np.float32)
-    out = []
-    for S in (2, 3, 4):
-        for t in range(64):
-            try:
-                with fd.Simulation(vel, 10.0, 5e-4, order,
-                                   options={fd.FD_OPT_RESIDENT: 1, fd.FD_OPT_TSTEPS: S, fdm.FD_OPT_TB2TILE: t}) as sim:
-                    sim.step(S)
-                    if sim.info()["tb_kind"] == 1:
-                        out.append((S, t))
-            except fdm.FDError:
-                pass
-    return out
 
 
 def main():
@@ -54,9 +37,8 @@ def main():
             tb += [{fd.FD_OPT_TSTEPS: 3}, {fd.FD_OPT_TSTEPS: 3, fd.FD_OPT_ZCHUNKS: 3}]
             if order == 2:
                 tb += [{fd.FD_OPT_TSTEPS: 4}]
-        if len(dims) == 2:                         # every register-streamed (rs2d) configuration
-            tb += [{fd.FD_OPT_TSTEPS: S, fd.FD_OPT_TB2TILE: t, fd.FD_OPT_ZCHUNKS: zc}
-                   for S, t in rs2d_tiles(fd, order) for zc in (0, 2)]
+        if len(dims) == 2 and order <= 4:          # rs2d defaults with a few warps (long runs, stealing)
+            tb += [{fd.FD_OPT_ZCHUNKS: 1}, {fd.FD_OPT_TSTEPS: 4 if order == 2 else 3, fd.FD_OPT_ZCHUNKS: 2}]
         # per-plane K (KZ variants) needs a layered model: the first half of
         # the planes at one velocity, the rest at another
         kz = [{fd.FD_OPT_KPLANE: 1, "layered": True}, {fd.FD_OPT_KPLANE: 1, fd.FD_OPT_TSTEPS: 1, "layered": True},
