@@ -35,13 +35,28 @@
 
 #include "fd_kernels.cuh"
 
+// Work stealing granularity defaults of CfgRS2 (A/B switches): claims of
+// FD_RS_CHK * U rows; a thief cuts a word with at least FD_RS_STEALMIN
+// claims' worth unclaimed
+#ifndef FD_RS_CHK
+#define FD_RS_CHK 2
+#endif
+#ifndef FD_RS_STEALMIN
+#define FD_RS_STEALMIN 2
+#endif
+
 namespace fdk {
 
 // R, S; HQ halo quads per side; W warps per CTA; Q rows in flight per warp
 // (shared-memory ring); MINB CTAs per SM.
-template <int R_, int S_, int HQ_, int W_, int Q_, int MINB_ = 1, bool TMA_ = true>
+template <int R_, int S_, int HQ_, int W_, int Q_, int MINB_ = 1, bool TMA_ = true, int CHK_ = FD_RS_CHK,
+          int SMIN_ = FD_RS_STEALMIN>
 struct CfgRS2 {
     static constexpr int R = R_, S = S_, HQ = HQ_, W = W_, Q = Q_, MINB = MINB_;
+    // work stealing: claims of CHK * U rows; a thief cuts a word with at
+    // least SMIN claims' worth unclaimed (r3 A/B on C2: order 2 S = 4 best at
+    // 1 / 2 -- 751 vs 722 Gpts/s at 2 / 2 --, order 4 S = 3 at 2 / 1: 641 vs 628)
+    static constexpr int CHK = CHK_, SMIN = SMIN_;
     // TMA: one lane loads each row's three 512 B pieces with bulk tensor copies
     // (cp.async.bulk.tensor, out-of-grid zero fill, one mbarrier per ring
     // slot); else every lane copies its own 16 B with cp.async (LDGSTS)
@@ -54,7 +69,7 @@ struct CfgRS2 {
     // rows per unrolled loop body = that length (no register moves)
     static constexpr int KQL = (KQ + 2 * R) / (2 * R + 1) * (2 * R + 1);
     static constexpr int U = KQL;
-    static constexpr int CH = 2 * U;                       // rows per work-stealing claim
+    static constexpr int CH = CHK * U;                     // rows per work-stealing claim
     static_assert(4 * HQ >= S * R, "the halo quads must cover S r columns");
     static_assert(S >= 2 && R >= 1 && R <= 4 && Q >= 2 && Q <= 16, "config");
 };
@@ -505,7 +520,7 @@ rs2d_step_kernel(const __grid_constant__ CUtensorMap map_p0,   // P^k buffer, bo
                 const int ob = __shfl_xor_sync(FULL, best, o), ol = __shfl_xor_sync(FULL, bl, o);
                 if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
             }
-            if (best < 2 * CH) { ++miss; continue; }
+            if (best < C::SMIN * CH) { ++miss; continue; }
             int m = 0, oend = 0, vunit = 0;
             if (lane == bl) {
                 m = nxt + (end - nxt) / 2;

@@ -10,9 +10,10 @@ FD_LAUNCHER(launch_rs2d, rs2d_step_kernel)
 // VARS: 0 = the band-rule kernel only, 1 = also the per-plane-K variant (the
 // S >= 3 defaults: single-slab contexts never run the sponge / peer
 // variants), 2 = all eight variants
-template <int R, int S, int HQ, int W, int Q, int MINB, int VARS, bool TMA>
+template <int R, int S, int HQ, int W, int Q, int MINB, int VARS, bool TMA, int CHK = FD_RS_CHK,
+          int SMIN = FD_RS_STEALMIN>
 static TileCfg make_rs2d() {
-    using C = CfgRS2<R, S, HQ, W, Q, MINB, TMA>;
+    using C = CfgRS2<R, S, HQ, W, Q, MINB, TMA, CHK, SMIN>;
     TileCfg t{2, R, C::TX, 1, W, Q, C::U, 128, 128, 1, 1, C::NTHREADS, C::SMEM_BYTES, {}, {}};
     if constexpr (VARS == 2) {
         FD_VARIANTS(t, C, true, rs2d_step_kernel, launch_rs2d);
