@@ -3,33 +3,35 @@
 //
 // In 2D a "plane" of the 2.5D scheme is one row, so the x taps of a row are
 // neighbouring lanes' registers and the z taps a per-thread register queue:
-// no shared memory, no TMA ring, no mbarriers.  One warp streams a column
-// strip down z: lane l holds the quad x = x0 - 4 HQ + 4 l .. + 3 of every
-// time level, 32 quads = 128 columns of which the middle TX = 4 (32 - 2 HQ)
-// are its own (the HQ halo quads on each side are recomputed by the
-// neighbouring strips: 4 HQ >= S r keeps the own quads exact after S steps).
-// Per row i the warp loads P^k(i), P^{k-1}(i - r), K(i - r) (cp.async, issued Q
-// rows ahead into a per-warp shared-memory ring) and evaluates Listing 3's run() body
-// S times, stage J (1..S) on row i - J r:
+// no stage tile in shared memory, no producer warp, no mbarriers between
+// stages.  One warp streams a column strip down z: lane l holds the quad
+// x = x0 - 4 HQ + 4 l .. + 3 of every time level, 32 quads = 128 columns of
+// which the middle TX = 4 (32 - 2 HQ) are its own (the HQ halo quads on each
+// side are recomputed by the neighbouring strips: 4 HQ >= S r keeps the own
+// quads exact after S steps).  Per row i the warp loads P^k(i), P^{k-1}(i - r),
+// K(i - r) into a per-warp shared-memory ring Q rows ahead (cp.async 16-B
+// copies, each lane its own quads; or, CfgRS2::TMA, three bulk tensor copies
+// by one lane) and evaluates Listing 3's run() body S times,
+// stage J (1..S) on row i - J r:
 //   P^{k+J} = fma(K, S(P^{k+J-1}), fma(2, P^{k+J-1}, -P^{k+J-2}))
 // with the eager injection of w_{k+J}; x taps by warp shuffle, z taps from
 // the level-(J-1) queue (2r + 1 rows), P^{k+J-2} from the level-(J-2) queue
 // (its oldest row) or, for J = 1, the P^{k-1} load.  Stages S-1 and S store
-// the own quads of the warp's rows [za, zb) to the C (P^{k+S-1}) and D
-// (P^{k+S}) buffers; every stage records its receivers (raw values).  Each
-// stage evaluates the canonical per-point expression (fd_kernels.cuh), so a
-// pass is bitwise S single steps.
+// the own quads of the run's rows to the C (P^{k+S-1}) and D (P^{k+S})
+// buffers; every stage records its receivers (raw values).  Each stage
+// evaluates the canonical per-point expression (fd_kernels.cuh), so a pass is
+// bitwise S single steps.
 //
 // HBM per pass: read P^k, P^{k-1}, K, write two levels: 20 B per point for S
-// updates.  Work unit = (column strip, z-chunk) as the tb2d kernel's chunked
-// mode with one-row blocks; the CTA's W warps split the chunk's rows.
+// updates.  Work: a persistent grid whose warps take equal row pieces of the
+// column strips, then balance by work stealing (rs2d_step_kernel).
 //
-// Rows outside the buffers (the warm-up rows of a chunk at the grid faces,
-// the U-padding of the unrolled loop) are loaded clamped and never stored;
-// rows outside the grid never reach a grid row (band rule, R#3: rows r..nz-r-1
-// are the only ones reading z taps).  Halos on z-slabs: S = 2 reads 2r planes
-// of P^k and r of P^{k-1} and K beyond the slab (the halo planes the runtime
-// exchanges); S >= 3 runs on single-slab contexts only.
+// Rows outside the buffers (the warm-up rows at the grid faces, the ring's
+// run-out) are zero-filled and never stored; rows outside the grid never
+// reach a grid row (band rule, R#3: rows r..nz-r-1 are the only ones reading
+// z taps).  Halos on z-slabs: S = 2 reads 2r planes of P^k and r of P^{k-1}
+// and K beyond the slab (the halo planes the runtime exchanges); S >= 3 runs
+// on single-slab contexts only.
 #pragma once
 #include <cstdio>
 
