@@ -352,7 +352,9 @@ __device__ __forceinline__ int rs2d_run(const StepParams &prm, const CUtensorMap
                 if (z == nzJ[J - 1] && z < c1)
                     nzJ[J - 1] = rs_record(o, z, u1, rpJ[J - 1], rend, x0 - 4 * HQ, prm.rec,
                                            trace_row_of(prm, kk + J - 1));
-                if (anysrc)                               // w_{k+J} at every computed point
+                // w_{k+J} at every computed point (the call only on the strip's
+                // source rows: an event block has S U stage rows)
+                if (anysrc && z >= src_lo && z <= src_hi)
                     o = rs_inject(o, z, smask, xb, J == S && own && z >= za && z < c1, prm,
                                   w_next_of(prm, kk + J - 1));
             }
